@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark of the ReCoVer data-parallel gradient commit on B200.
+
+Workload (BASELINE.json configs[1]): the GPT-2 124M gradient
+(d = 124,439,808 fp32 = 497.8 MB), DP = 8 replicas, M = 32 microbatches per
+optimizer step (G = 4 per replica), K = 20 buckets (~25 MB), replica 3 killed
+``during_sync`` on bucket 7 in the middle of the timed region.  At N=1 the
+eight replicas live on one GPU (the reference's own single-process model).
+
+A "step" is one optimizer step's gradient commit: the fused canonical-order
+accumulate + survivor-masked reduce + 1/M scale of all 32 microbatch
+gradients (synthetic, resident in HBM; they stand for the backward outputs)
+into every live replica's gradient buffer, through GradientCommit.step with
+the failure schedule, recovery included.
+
+Metric: committed tokens/s (tokens_per_microbatch = 4096, sim.py:230) under
+the failure schedule; the line also carries the commit kernel's HBM GB/s vs
+the measured peak (roofline) and recovery ms.  ``--impl reference`` times the
+reference algorithm (the oracle port of comm.py/trainer.py: per-replica
+`flat += grad`, snapshot copies, ascending masked fold, rewinds) on the host
+cores over a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+D_GPT2 = 124_439_808
+W, G, K = 8, 4, 20
+M = W * G
+TOKENS_PER_MB = 4096
+VICTIM, VICTIM_BUCKET = 3, 7
+METRIC = "committed tokens/s under failure schedule; masked-allreduce GB/s; recovery ms"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--numel", type=int, default=D_GPT2)
+    ap.add_argument("--no-fail", action="store_true")
+    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 23)
+    ap.add_argument("--skip-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+class StepKill:
+    """Kill VICTIM during_sync on VICTIM_BUCKET at one step (configs[1])."""
+
+    def __init__(self, at_step):
+        self.at_step = at_step
+        self.step = -1
+
+    def fire(self, phase, bucket=None):
+        if self.step == self.at_step and phase == "during_sync" and bucket == VICTIM_BUCKET:
+            return [VICTIM]
+        return []
+
+
+# ---------------------------------------------------------------------------
+# CPU legs: the reference algorithm (oracle port) on a bounded sample
+
+def _threads():
+    return max(1, os.cpu_count() or 1)
+
+
+def _chunked(n, fn):
+    """Run fn(lo, hi) over n elements split across all host threads (numpy
+    releases the GIL inside ufuncs)."""
+    nt = _threads()
+    edges = [n * i // nt for i in range(nt + 1)]
+    ths = [threading.Thread(target=fn, args=(edges[i], edges[i + 1])) for i in range(nt)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    return nt
+
+
+def reference_step_sample(leaves, fail_bucket=None):
+    """One optimizer step of the reference's data path on a sample:
+    trainer.py:192,212 (zero + `flat += grad` per round), buckets.py:68
+    (snapshot copies), comm.py:191-200 (ascending fold, write all members),
+    on failure buckets.py:136 (rewinds) and the extension pass, then
+    trainer.py:446 (`flat / B`)."""
+    import numpy as np
+    from oracle import fold
+    n = leaves[0].shape[0]
+    kb = K
+    bounds = [(i * (n // kb), n if i == kb - 1 else (i + 1) * (n // kb)) for i in range(kb)]
+    flats = [np.zeros(n, dtype=np.float32) for _ in range(W)]
+    snaps = [np.empty(n, dtype=np.float32) for _ in range(W)]
+
+    def run(lo, hi):
+        for r in range(W):
+            for j in range(G):
+                flats[r][lo:hi] += leaves[r * G + j][lo:hi]
+        members = list(range(W))
+
+        def cascade(ks, mem):
+            for k in ks:
+                a, b = bounds[k]
+                a, b = max(a, lo), min(b, hi)
+                if a >= b:
+                    continue
+                for r in mem:
+                    snaps[r][a:b] = flats[r][a:b]
+                tot = fold.masked_fold([flats[r][a:b] for r in mem], [True] * len(mem))
+                for r in mem:
+                    flats[r][a:b] = tot
+        if fail_bucket is None:
+            cascade(range(kb), members)
+        else:
+            cascade(range(fail_bucket), members)
+            members = [r for r in members if r != VICTIM]
+            for k in range(fail_bucket + 1):          # rewind stale buckets
+                a, b = bounds[k]
+                a, b = max(a, lo), min(b, hi)
+                for r in members:
+                    if a < b:
+                        flats[r][a:b] = snaps[r][a:b]
+            for r in members[:4]:                      # g_ext=1, 3 boundary minors
+                flats[r][lo:hi] += leaves[VICTIM * G + members.index(r)][lo:hi]
+            cascade(range(kb), members)
+        upd = flats[members[0]][lo:hi] / np.float32(M)
+        del upd
+
+    return _chunked(n, run)
+
+
+def cpu_leg(sample, steps, fail_index):
+    """Time the reference algorithm on `sample` elements per step; scale to
+    the full gradient.  Returns (tokens/s, seconds per full step, threads)."""
+    import numpy as np
+    rng = np.random.default_rng(1234)
+    leaves = [rng.standard_normal(sample, dtype=np.float32) for _ in range(M)]
+    reference_step_sample(leaves)  # warm caches / page in
+    t0 = time.perf_counter()
+    nt = 1
+    for s in range(steps):
+        nt = reference_step_sample(leaves, VICTIM_BUCKET if s == fail_index else None)
+    dt = time.perf_counter() - t0
+    per_full = dt / steps * (D_GPT2 / sample)
+    return M * TOKENS_PER_MB / per_full, per_full, nt
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = max(1, min(args.steps, 3))
+    tps, per_full, nt = cpu_leg(args.cpu_sample, steps, steps // 2 if not args.no_fail else -1)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": 1,
+        "ms_per_step": per_full * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "gpt2-124m gradient commit, DP=8, M=32, K=20, "
+                               "replica 3 killed during_sync:7", "numel": D_GPT2,
+                   "replicas": W, "microbatches": M, "buckets": K},
+        "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": nt, "kind": "port",
+                         "sample": "%d of %d elements per step, %d steps, scaled linearly"
+                                   % (args.cpu_sample, D_GPT2, steps)},
+        "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+def run_ours(args):
+    import torch
+    from paper_2605_11215_b200.commit import GradientCommit
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    numel = args.numel
+
+    # synthetic per-microbatch gradients (the backward outputs), in HBM
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    leaves = [torch.randn(numel, generator=gen, device=dev, dtype=torch.float32)
+              for _ in range(M)]
+    total_steps = args.warmup + args.steps
+    fail_step = -1 if args.no_fail else args.warmup + args.steps // 2
+    eng = GradientCommit(numel, W, G, K, placement={r: dev for r in range(W)},
+                         variant=args.variant)
+    kill = StepKill(fail_step)
+
+    def leaf(m, rid):
+        return leaves[m]
+
+    # reference layout of the group for the e2e leg is identical; warm up
+    stream = torch.cuda.current_stream(dev)
+    step_ev = []
+    outcomes = []
+    launches = 0
+    for s in range(args.warmup):
+        kill.step = s
+        eng.step(s, leaf, kill)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    eng.timing = []
+    with Clocks(local) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for s in range(args.warmup, total_steps):
+            kill.step = s
+            a = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            out = eng.step(s, leaf, kill)
+            outcomes.append(out)
+            launches += out.launches
+            step_ev.append(a)
+        end.record(stream)
+        torch.cuda.synchronize()
+    elapsed_ms = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    step_ev.append(end)
+    step_ms = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(len(step_ev) - 1)]
+    committed = sum(o.contrib_total for o in outcomes)
+    tokens = committed * TOKENS_PER_MB
+    value = tokens / (elapsed_ms / 1e3)
+
+    # roofline of the fused commit kernel over the timed region
+    durs = [a.elapsed_time(z) for a, z, _ in eng.timing]
+    nbytes = [b for _, _, b in eng.timing]
+    achieved = sum(nbytes) / (sum(durs) / 1e3) / 1e9 if durs else None
+    peak, peak_kind = peaks()
+    fail_idx = [i for i, o in enumerate(outcomes) if o.events]
+    normal = [ms for i, ms in enumerate(step_ms) if i not in fail_idx]
+    recovery_ms = (step_ms[fail_idx[0]] - statistics.median(normal)) if fail_idx and normal else None
+    eng.timing = None
+
+    # correctness spot check inside the bench: every live replica holds the
+    # same bytes (one kernel wrote them all)
+    ref = eng.grads[eng.comm.members[0]]
+    agree = all(torch.equal(eng.grads[r], ref) for r in eng.comm.members[1:])
+
+    # e2e through the public API with host buffers: pinned host gradients
+    # copied in every step, committed gradient copied out every step
+    e2e = None
+    if args.e2e_steps > 0:
+        e2e = e2e_leg(args, dev, leaves, numel)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": "gpt2-124m gradient commit, DP=8, M=32, K=20, "
+                               "replica 3 killed during_sync:7",
+                   "numel": numel, "replicas": W, "microbatches": M, "buckets": K,
+                   "tokens_per_microbatch": TOKENS_PER_MB,
+                   "fail_step": fail_step, "placement": "8 replicas on 1 GPU" if world == 1
+                   else "replicas per rank", "l2": "inputs 15.9 GB >> 126 MB L2",
+                   "parallelism": "dp8-sim"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "peak_kind": peak_kind, "kernel": "fold_tma_kernel (rcv_tree_commit)",
+                     "launches_timed": len(durs),
+                     "mean_launch_us": 1e3 * sum(durs) / len(durs) if durs else None},
+        "allreduce_gbs": achieved,
+        "recovery_ms": recovery_ms,
+        "step_ms": {"median": statistics.median(step_ms), "max": max(step_ms),
+                    "failure_step": step_ms[fail_idx[0]] if fail_idx else None},
+        "replica_agreement": agree,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if rank == 0 and not args.skip_cpu:
+        tps, per_full, nt = cpu_leg(args.cpu_sample, 2, 1)
+        line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": nt, "kind": "port",
+                                "sample": "%d of %d elements per step, 2 steps (one with "
+                                          "the failure), scaled linearly" % (args.cpu_sample, D_GPT2)}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def e2e_leg(args, dev, leaves, numel):
+    """Same step through GradientCommit with HOST inputs: every step copies
+    the 32 microbatch gradients host->device (pinned) and the committed
+    gradient device->host, inside the timed region."""
+    import torch
+    from paper_2605_11215_b200.commit import GradientCommit
+    try:
+        host = [torch.empty(numel, dtype=torch.float32, pin_memory=True) for _ in range(M)]
+        pinned = True
+    except RuntimeError:
+        host = [torch.empty(numel, dtype=torch.float32) for _ in range(M)]
+        pinned = False
+    for h, l in zip(host, leaves):
+        h.copy_(l)
+    out_host = torch.empty(numel, dtype=torch.float32, pin_memory=pinned)
+    eng = GradientCommit(numel, W, G, K, placement={r: dev for r in range(W)})
+    dev_slots = leaves  # reuse the HBM slots as H2D targets
+    stream = torch.cuda.current_stream(dev)
+
+    def one(s):
+        for h, d in zip(host, dev_slots):
+            d.copy_(h, non_blocking=True)
+        eng.step(s, lambda m, rid: dev_slots[m])
+        out_host.copy_(eng.grads[eng.comm.members[0]], non_blocking=True)
+
+    one(0)
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    z = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for s in range(args.e2e_steps):
+        one(s + 1)
+    z.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(z) / args.e2e_steps
+    bi = M * numel * 4
+    bo = numel * 4
+    return {"value": M * TOKENS_PER_MB / (ms / 1e3), "unit": "tokens/s",
+            "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "ms_per_step": ms,
+            "steps": args.e2e_steps, "pinned": pinned,
+            "h2d_gbs": (bi + bo) / (ms / 1e3) / 1e9}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

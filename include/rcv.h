@@ -1,0 +1,181 @@
+/*
+ * rcv.h — C ABI of librcv.so, the B200 (sm_100a) data plane of the ReCoVer
+ * data-parallel gradient commit.
+ *
+ * The reference (`steadybatch`, /root/reference/pkg/src/steadybatch) is a pure
+ * Python/numpy package; its "FFI" for this path is the Python module API.  Each
+ * entry point below names the reference operation whose data movement it
+ * replaces (file:line under pkg/src/steadybatch/).  The control plane
+ * (membership, epoch, roles, quotas) stays in the host mirror of that API
+ * (paper_2605_11215_b200/{comm,buckets,policy,trainer}.py), which calls these
+ * functions through ctypes.
+ *
+ * Conventions
+ *   - every function returns 0 on success, a negative RCV_E* code otherwise;
+ *     rcv_last_error() returns a thread-local message for the last failure.
+ *   - all buffers are caller-owned device pointers (UVA: a pointer may live on
+ *     a peer GPU when peer access is enabled, see rcv_enable_peer_access).
+ *   - every call is stream-ordered on the caller's cudaStream_t (`stream`,
+ *     passed as void*); nothing synchronises the host.
+ *   - dtypes: RCV_F32, RCV_F64 (accumulator / output types) and RCV_BF16
+ *     (input-only: bf16 gradients accumulated in fp32).
+ *   - floating-point folds are evaluated in the exact association order the
+ *     function documents; no reassociation, no FMA contraction, the final
+ *     scale is an IEEE true division (x / divisor), matching numpy.
+ */
+#ifndef RCV_H_
+#define RCV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RCV_F32 0
+#define RCV_F64 1
+#define RCV_BF16 2
+
+#define RCV_OK 0
+#define RCV_EINVAL (-1)
+#define RCV_ECUDA (-2)
+#define RCV_ERANGE (-3)
+
+#define RCV_MAX_IN 64  /* max fold inputs (replicas / microbatch slots) */
+#define RCV_MAX_OUT 64 /* max fold outputs (member views)               */
+
+/* fold op byte (one per input, see rcv_fold): bits 0-5 = number of merges of
+ * the two top stack entries after pushing this input; bit 6 = push +0.0 + v
+ * instead of v (reproduces numpy's `zeros; +=`, which turns -0.0 into +0.0). */
+#define RCV_OP_MERGES_MASK 0x3f
+#define RCV_OP_CANON 0x40
+
+/* kernel variant selector for rcv_fold / rcv_tree_commit */
+#define RCV_VARIANT_AUTO 0
+#define RCV_VARIANT_TMA 1    /* cp.async.bulk → smem ring → fold → STG.128 */
+#define RCV_VARIANT_DIRECT 2 /* LDG.128 with prefetch, fold in registers  */
+#define RCV_VARIANT_SCALAR 3 /* one element per thread (any alignment)    */
+
+const char *rcv_last_error(void);
+int rcv_version(void);
+
+/* Number of CUDA devices visible (0 without a GPU; never fails on CPU). */
+int rcv_device_count(int *n);
+
+/* Enable peer access between every ordered pair of `devices` (single-process
+ * multi-GPU mode).  Replaces nothing in the reference (its replicas share one
+ * address space, comm.py:1-9); it is what makes views on different GPUs
+ * addressable from one kernel. */
+int rcv_enable_peer_access(int n_dev, const int *devices);
+
+/* Generic ordered fold — the single data-plane primitive.
+ *   For every element e in [0, numel): run the stack program
+ *     for i in 0..n_in-1: push(in[i][e]) (as +0.0+v when ops[i] & CANON);
+ *                         repeat (ops[i] & MERGES) times: b=pop, a=pop, push(a+b)
+ *   the single remaining value v becomes v / divisor when divisor != 0, and is
+ *   written to out[0..n_out-1][e].
+ *   in_dtypes[i] is acc_dtype or (acc_dtype == F32 only) RCV_BF16.
+ *   Outputs may alias inputs (each element is read completely before it is
+ *   written).  n_in == 0 writes +0.0 (np.zeros_like, comm.py:197-198). */
+int rcv_fold(int n_in, const void *const *in, const uint8_t *ops,
+             const int *in_dtypes, int n_out, void *const *out, int acc_dtype,
+             size_t numel, double divisor, int variant, void *stream);
+
+/* Communicator.ulfm_allreduce data phase (comm.py:191-200): the views of the
+ * `n` members in ascending replica id; bit i of contrib_mask set ⇔ member i
+ * contributes (non-spare, or any member while boundary_latch, comm.py:193).
+ * total = left fold over contributors in ascending order, starting from the
+ * first contributor's value (comm.py:196 `vec.copy()`, so -0.0 survives);
+ * every member's view (spares included) receives total (comm.py:199-200), or
+ * +0.0 when nobody contributes.  divisor != 0 additionally scales (used by the
+ * fused commit, trainer.py:446). In place. */
+int rcv_masked_allreduce(void *const *views, int n, uint64_t contrib_mask,
+                         int dtype, size_t numel, double divisor,
+                         void *stream);
+
+/* Same, with the members' views spread over several GPUs of this process
+ * (peer access enabled).  Device d folds the d-th contiguous 16-byte-aligned
+ * slice of the bucket, reading every contributor's slice over NVLink and
+ * writing every member's slice (a fused reduce-scatter + all-gather in one
+ * launch per device).  streams[d] is the stream for devices[d]; the call
+ * orders all streams before and after with events. */
+int rcv_masked_allreduce_multidev(void *const *views, int n,
+                                  uint64_t contrib_mask, int dtype,
+                                  size_t numel, double divisor, int n_dev,
+                                  const int *devices, void *const *streams);
+
+/* ReplicaState.execute_microbatch accumulation `self.flat += grad`
+ * (trainer.py:212, 225): acc = acc + grad, or +0.0 + grad when `first`
+ * (folds the `flat[:] = 0.0` of begin_iteration, trainer.py:192, into the
+ * first push).  grad_dtype may be RCV_BF16 when acc_dtype is RCV_F32. */
+int rcv_accumulate(void *acc, const void *grad, int acc_dtype, int grad_dtype,
+                   size_t numel, int first, void *stream);
+
+/* Canonical-order commit (the B200 design): `blocks` are
+ * partial sums of aligned dyadic microbatch-index blocks [lo, lo+2^level)
+ * over a canonical binary tree of next_pow2(n_leaves) leaves, empty leaves
+ * skipped (not added as zeros).  The kernel evaluates that tree in
+ * post-order, divides by divisor (trainer.py:446 `flat / B`), and writes
+ * every out[j].  The result is a function of the leaf values only, never of
+ * which replica computed which block. */
+typedef struct {
+  const void *ptr;
+  uint32_t lo;
+  uint32_t level;
+  int dtype;
+} rcv_block;
+int rcv_tree_commit(const rcv_block *blocks, int n_blocks, uint32_t n_leaves,
+                    int n_out, void *const *out, int acc_dtype, size_t numel,
+                    double divisor, int variant, void *stream);
+
+/* Host-side helper: the post-order fold program for rcv_tree_commit, exposed
+ * so tests can check it without a GPU.  ops_out must hold n_blocks bytes;
+ * blocks are taken in ascending `lo` order (the caller sorts). Returns the
+ * maximum stack depth in *max_depth. */
+int rcv_tree_program(const uint32_t *lo, const uint32_t *level, int n_blocks,
+                     uint32_t n_leaves, uint8_t *ops_out, int *max_depth);
+
+/* snapshot_and_tag deep copy (buckets.py:68) and rewinds (buckets.py:136,
+ * 162): device-to-device copy. */
+int rcv_copy(void *dst, const void *src, size_t bytes, void *stream);
+
+/* begin_iteration `flat[:] = 0.0` (trainer.py:192) and the spare discard
+ * `b.data[:] = 0.0` (buckets.py:147-148). */
+int rcv_zero(void *dst, size_t bytes, void *stream);
+
+/* np.array_equal between replica buffers (trainer.py:441-444, 451-453):
+ * adds the number of differing 32-bit words of a and b to *d_count (a device
+ * uint64).  Bitwise, so -0.0 != +0.0 and NaN payloads compare by bits. */
+int rcv_compare(const void *a, const void *b, size_t bytes,
+                unsigned long long *d_count, void *stream);
+
+/* The optimizer commit `params -= lr * (flat / float(b))` (trainer.py:450),
+ * evaluated as three IEEE roundings in numpy's order. */
+int rcv_sgd_commit(void *params, const void *flat, int dtype, size_t numel,
+                   double b, double lr, void *stream);
+
+/* Deterministic example synthesis (trainer.py:64-87), a bit-exact device port
+ * of _unit_lanes:  out[l] = ((mix64(base + l*C1) >> 11) * 2^-53) * scale +
+ * shift for l in [0, n), all in float64; then, when floor7 != 0, out[l] =
+ * floor(out[l] * 7.0) - 3.0 (the constant stream's g0, trainer.py:152).
+ * base = seed*C1 + index*C2 + salt*C3 mod 2^64 is computed by the caller. */
+int rcv_unit_lanes(double *out, uint64_t base, size_t n, double scale,
+                   double shift, int floor7, void *stream);
+
+/* Toy-model gradient and loss (trainer.py:103-131) for one example:
+ *   linear:   r = params.x - y ; grad = r * x ; loss = r * r
+ *   constant: grad = x         ; loss = params.x
+ * where x = lanes[0:dim], and for linear y = wstar.x + 0.1*lanes[dim]
+ * (trainer.py:165-168).  Dot products are a fixed-order sequential fold.
+ * grad (dim doubles; may be NULL to compute the loss only) and scal (two
+ * doubles: scal[0] = r for linear / 1.0 for constant, scal[1] = loss) are
+ * device outputs. */
+int rcv_toy_grad(int kind_linear, const double *params, const double *lanes,
+                 const double *wstar, size_t dim, double *grad, double *scal,
+                 void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RCV_H_ */

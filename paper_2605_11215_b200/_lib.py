@@ -1,0 +1,305 @@
+"""ctypes binding of librcv.so (include/rcv.h) plus thin tensor-level helpers.
+
+This is the only place the package touches the native library.  There is no
+CPU fallback: if the library is missing, or a data-plane call is made on a
+tensor that is not on a CUDA device, the call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import torch
+
+F32, F64, BF16 = 0, 1, 2
+OP_CANON = 0x40
+VARIANT_AUTO, VARIANT_TMA, VARIANT_DIRECT, VARIANT_SCALAR = 0, 1, 2, 3
+MAX_IN = 64
+MAX_OUT = 64
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librcv.so")
+
+# every symbol include/rcv.h declares (tests check the export table)
+EXPORTS = (
+    "rcv_last_error", "rcv_version", "rcv_device_count",
+    "rcv_enable_peer_access", "rcv_fold", "rcv_masked_allreduce",
+    "rcv_masked_allreduce_multidev", "rcv_accumulate", "rcv_tree_commit",
+    "rcv_tree_program", "rcv_copy", "rcv_zero", "rcv_compare",
+    "rcv_sgd_commit", "rcv_unit_lanes", "rcv_toy_grad",
+)
+
+
+class RcvError(RuntimeError):
+    """A librcv.so call returned an error code."""
+
+
+class _Block(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("lo", ctypes.c_uint32),
+                ("level", ctypes.c_uint32), ("dtype", ctypes.c_int)]
+
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RcvError(
+            "librcv.so not built (%s); run __graft_entry__.build() or "
+            "`make -C paper_2605_11215_b200/csrc`" % LIB_PATH)
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, sz, i32, u64, u32 = (ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
+                             ctypes.c_uint64, ctypes.c_uint32)
+    pvp = ctypes.POINTER(ctypes.c_void_p)
+    sig = {
+        "rcv_last_error": (ctypes.c_char_p, []),
+        "rcv_version": (i32, []),
+        "rcv_device_count": (i32, [ctypes.POINTER(i32)]),
+        "rcv_enable_peer_access": (i32, [i32, ctypes.POINTER(i32)]),
+        "rcv_fold": (i32, [i32, pvp, ctypes.POINTER(ctypes.c_uint8),
+                           ctypes.POINTER(i32), i32, pvp, i32, sz,
+                           ctypes.c_double, i32, vp]),
+        "rcv_masked_allreduce": (i32, [pvp, i32, u64, i32, sz,
+                                       ctypes.c_double, vp]),
+        "rcv_masked_allreduce_multidev": (i32, [pvp, i32, u64, i32, sz,
+                                                ctypes.c_double, i32,
+                                                ctypes.POINTER(i32), pvp]),
+        "rcv_accumulate": (i32, [vp, vp, i32, i32, sz, i32, vp]),
+        "rcv_tree_commit": (i32, [ctypes.POINTER(_Block), i32, u32, i32, pvp,
+                                  i32, sz, ctypes.c_double, i32, vp]),
+        "rcv_tree_program": (i32, [ctypes.POINTER(u32), ctypes.POINTER(u32),
+                                   i32, u32, ctypes.POINTER(ctypes.c_uint8),
+                                   ctypes.POINTER(i32)]),
+        "rcv_copy": (i32, [vp, vp, sz, vp]),
+        "rcv_zero": (i32, [vp, sz, vp]),
+        "rcv_compare": (i32, [vp, vp, sz, vp, vp]),
+        "rcv_sgd_commit": (i32, [vp, vp, i32, sz, ctypes.c_double,
+                                 ctypes.c_double, vp]),
+        "rcv_unit_lanes": (i32, [vp, u64, sz, ctypes.c_double,
+                                 ctypes.c_double, i32, vp]),
+        "rcv_toy_grad": (i32, [i32, vp, vp, vp, sz, vp, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = load().rcv_last_error().decode(errors="replace")
+        raise RcvError("librcv error %d: %s" % (rc, msg))
+
+
+# ---- tensor helpers --------------------------------------------------------
+
+_DT = {torch.float32: F32, torch.float64: F64, torch.bfloat16: BF16}
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise TypeError("unsupported dtype %s (float32/float64/bfloat16)"
+                        % t.dtype) from None
+
+
+def require_cuda(t: torch.Tensor, what: str = "tensor") -> None:
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("%s must be a torch.Tensor on a CUDA device, got %r"
+                        % (what, type(t).__name__))
+    if not t.is_cuda:
+        raise RcvError("%s is on %s: the data plane runs only on CUDA devices "
+                       "(no CPU fallback)" % (what, t.device))
+    if t.dim() != 1 or not t.is_contiguous():
+        raise ValueError("%s must be a contiguous 1-D view" % what)
+
+
+def stream_of(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _ptrs(ts: Sequence[torch.Tensor]):
+    arr = (ctypes.c_void_p * max(1, len(ts)))()
+    for i, t in enumerate(ts):
+        arr[i] = t.data_ptr()
+    return arr
+
+
+def fold(inputs: Sequence[torch.Tensor], ops: Sequence[int],
+         outputs: Sequence[torch.Tensor], divisor: float = 0.0,
+         variant: int = VARIANT_AUTO, stream: Optional[int] = None) -> None:
+    """rcv_fold over torch tensors (all on one device, same numel)."""
+    if not outputs:
+        return
+    acc = outputs[0]
+    for t in list(inputs) + list(outputs):
+        require_cuda(t)
+        if t.numel() != acc.numel():
+            raise ValueError("fold operands differ in length")
+    n_in = len(inputs)
+    opa = (ctypes.c_uint8 * max(1, n_in))(*ops)
+    dta = (ctypes.c_int * max(1, n_in))(*[dtype_code(t) for t in inputs])
+    _check(load().rcv_fold(n_in, _ptrs(inputs), opa, dta, len(outputs),
+                           _ptrs(outputs), dtype_code(acc), acc.numel(),
+                           float(divisor), variant,
+                           stream if stream is not None else stream_of(acc)))
+
+
+def masked_allreduce(views: Sequence[torch.Tensor], contrib: Sequence[bool],
+                     divisor: float = 0.0) -> None:
+    """rcv_masked_allreduce (same device) or the multi-device variant."""
+    lib = load()
+    n = len(views)
+    if n == 0:
+        return
+    first = views[0]
+    for v in views:
+        require_cuda(v, "bucket view")
+        if v.dtype != first.dtype or v.numel() != first.numel():
+            raise ValueError("bucket views differ in dtype or length")
+    mask = 0
+    for i, c in enumerate(contrib):
+        if c:
+            mask |= 1 << i
+    code = dtype_code(first)
+    if code == BF16:
+        raise TypeError("bucket views hold accumulators: float32 or float64")
+    devs = sorted({v.device.index for v in views})
+    if len(devs) == 1:
+        _check(lib.rcv_masked_allreduce(_ptrs(views), n, mask, code,
+                                        first.numel(), float(divisor),
+                                        stream_of(first)))
+        return
+    dev_arr = (ctypes.c_int * len(devs))(*devs)
+    streams = (ctypes.c_void_p * len(devs))(
+        *[torch.cuda.current_stream(d).cuda_stream for d in devs])
+    _check(lib.rcv_masked_allreduce_multidev(
+        _ptrs(views), n, mask, code, first.numel(), float(divisor),
+        len(devs), dev_arr, streams))
+
+
+_peer_done: set = set()
+
+
+def enable_peer_access(devices: Sequence[int]) -> None:
+    key = tuple(sorted(set(devices)))
+    if len(key) < 2 or key in _peer_done:
+        return
+    arr = (ctypes.c_int * len(key))(*key)
+    _check(load().rcv_enable_peer_access(len(key), arr))
+    _peer_done.add(key)
+
+
+def accumulate(acc: torch.Tensor, grad: torch.Tensor, first: bool = False) -> None:
+    require_cuda(acc, "accumulator")
+    require_cuda(grad, "gradient")
+    if acc.numel() != grad.numel():
+        raise ValueError("accumulator and gradient differ in length")
+    _check(load().rcv_accumulate(acc.data_ptr(), grad.data_ptr(),
+                                 dtype_code(acc), dtype_code(grad),
+                                 acc.numel(), int(first), stream_of(acc)))
+
+
+def tree_program(blocks: Sequence[tuple], n_leaves: int):
+    """(lo, level) blocks in ascending lo -> (ops bytes, max depth)."""
+    n = len(blocks)
+    lo = (ctypes.c_uint32 * max(1, n))(*[b[0] for b in blocks])
+    lev = (ctypes.c_uint32 * max(1, n))(*[b[1] for b in blocks])
+    ops = (ctypes.c_uint8 * max(1, n))()
+    depth = ctypes.c_int(0)
+    _check(load().rcv_tree_program(lo, lev, n, n_leaves, ops,
+                                   ctypes.byref(depth)))
+    return list(ops)[:n], depth.value
+
+
+def tree_commit(blocks: Sequence[tuple], n_leaves: int,
+                outputs: Sequence[torch.Tensor], divisor: float,
+                variant: int = VARIANT_AUTO) -> None:
+    """blocks: sequence of (tensor, lo, level), ascending lo."""
+    if not outputs:
+        return
+    acc = outputs[0]
+    arr = (_Block * max(1, len(blocks)))()
+    for i, (t, lo, level) in enumerate(blocks):
+        require_cuda(t, "block partial")
+        if t.numel() != acc.numel():
+            raise ValueError("block partial length differs from the output")
+        arr[i] = _Block(t.data_ptr(), lo, level, dtype_code(t))
+    for o in outputs:
+        require_cuda(o, "commit output")
+    _check(load().rcv_tree_commit(arr, len(blocks), n_leaves, len(outputs),
+                                  _ptrs(outputs), dtype_code(acc),
+                                  acc.numel(), float(divisor), variant,
+                                  stream_of(acc)))
+
+
+def copy_(dst: torch.Tensor, src: torch.Tensor) -> None:
+    require_cuda(dst, "copy destination")
+    require_cuda(src, "copy source")
+    if dst.numel() != src.numel() or dst.dtype != src.dtype:
+        raise ValueError("copy operands differ")
+    _check(load().rcv_copy(dst.data_ptr(), src.data_ptr(),
+                           dst.numel() * dst.element_size(), stream_of(dst)))
+
+
+def zero_(dst: torch.Tensor) -> None:
+    require_cuda(dst, "zero target")
+    _check(load().rcv_zero(dst.data_ptr(), dst.numel() * dst.element_size(),
+                           stream_of(dst)))
+
+
+def count_differences(a: torch.Tensor, b: torch.Tensor,
+                      counter: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Device uint64 (as int64 tensor) count of differing 32-bit words."""
+    require_cuda(a)
+    require_cuda(b)
+    if a.numel() * a.element_size() != b.numel() * b.element_size():
+        return torch.ones((), dtype=torch.int64, device=a.device)
+    if counter is None:
+        counter = torch.zeros((), dtype=torch.int64, device=a.device)
+    _check(load().rcv_compare(a.data_ptr(), b.data_ptr(),
+                              a.numel() * a.element_size(),
+                              counter.data_ptr(), stream_of(a)))
+    return counter
+
+
+def sgd_commit(params: torch.Tensor, flat: torch.Tensor, b: float,
+               lr: float) -> None:
+    require_cuda(params, "params")
+    require_cuda(flat, "flat gradient")
+    if params.dtype != flat.dtype or params.numel() != flat.numel():
+        raise ValueError("params/flat mismatch")
+    _check(load().rcv_sgd_commit(params.data_ptr(), flat.data_ptr(),
+                                 dtype_code(params), params.numel(),
+                                 float(b), float(lr), stream_of(params)))
+
+
+def unit_lanes(out: torch.Tensor, base: int, scale: float = 1.0,
+               shift: float = 0.0, floor7: bool = False) -> None:
+    require_cuda(out, "lanes")
+    if out.dtype != torch.float64:
+        raise TypeError("lanes are float64")
+    _check(load().rcv_unit_lanes(out.data_ptr(), base & ((1 << 64) - 1),
+                                 out.numel(), float(scale), float(shift),
+                                 int(floor7), stream_of(out)))
+
+
+def toy_grad(linear: bool, params: torch.Tensor, lanes: torch.Tensor,
+             wstar: Optional[torch.Tensor], grad: torch.Tensor,
+             scal: torch.Tensor) -> None:
+    for t in (params, lanes, grad, scal):
+        require_cuda(t)
+    dim = params.numel()
+    _check(load().rcv_toy_grad(int(linear), params.data_ptr(),
+                               lanes.data_ptr(),
+                               wstar.data_ptr() if wstar is not None else None,
+                               dim, grad.data_ptr(), scal.data_ptr(),
+                               stream_of(grad)))

@@ -1,0 +1,1109 @@
+// librcv.so — sm_100a data plane of the ReCoVer gradient commit.
+//
+// One primitive does all floating-point work on the path: an ordered stack
+// fold of n_in input buffers into n_out output buffers (rcv_fold, see
+// include/rcv.h).  The reference's three data-movement sites are all folds:
+//   * Communicator.ulfm_allreduce   comm.py:191-200   left fold over contributors,
+//                                                     broadcast to every member
+//   * execute_microbatch `+=`       trainer.py:212,225  acc + grad
+//   * commit `flat / B`             trainer.py:446     fold of one input + divide
+// and the B200-only canonical commit (dyadic tree over microbatch indices) is a
+// post-order fold program.  The work is HBM/NVLink-bandwidth bound (one add
+// per 4-8 bytes moved), so there are no tensor cores here: the kernels are
+// built around keeping enough bytes in flight.
+//
+// Variants (chosen per call, RCV_VARIANT_*):
+//   TMA    one producer warp streams every input's tile into a shared-memory
+//          ring with cp.async.bulk (UBLKCP) + mbarrier complete_tx; four
+//          consumer warps run the fold out of shared memory and store with
+//          128-bit STG.  Bytes in flight are set by the ring depth, not by
+//          registers, so it holds HBM/NVLink busy for any n_in.
+//   DIRECT 128-bit LDG with one-input-ahead prefetch and U independent vectors
+//          per thread, fold in registers.
+//   SCALAR one element per thread; heads/tails and misaligned views.
+//
+// Fold order is exact: every add is __fadd_rn/__dadd_rn in program order,
+// the final scale is __fdiv_rn/__ddiv_rn (IEEE true division, like numpy).
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rcv.h"
+
+#define RCV_VERSION 1
+
+// ---------------------------------------------------------------------------
+// errors
+
+static thread_local std::string g_err;
+
+static int set_err(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                              \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      return set_err(RCV_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,    \
+                     cudaGetErrorString(e_));                                 \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// device helpers
+
+template <typename A> struct VecT;
+template <> struct VecT<float> {
+  using V = float4;
+  static constexpr int E = 4;  // elements per 16-byte vector
+};
+template <> struct VecT<double> {
+  using V = double2;
+  static constexpr int E = 2;
+};
+
+__device__ __forceinline__ float4 vadd(const float4 &a, const float4 &b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y),
+                     __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+__device__ __forceinline__ double2 vadd(const double2 &a, const double2 &b) {
+  return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+__device__ __forceinline__ float4 vcanon(const float4 &a) {
+  return vadd(make_float4(0.f, 0.f, 0.f, 0.f), a);
+}
+__device__ __forceinline__ double2 vcanon(const double2 &a) {
+  return vadd(make_double2(0.0, 0.0), a);
+}
+__device__ __forceinline__ float4 vdiv(const float4 &a, double d) {
+  const float f = (float)d;
+  return make_float4(__fdiv_rn(a.x, f), __fdiv_rn(a.y, f), __fdiv_rn(a.z, f),
+                     __fdiv_rn(a.w, f));
+}
+__device__ __forceinline__ double2 vdiv(const double2 &a, double d) {
+  return make_double2(__ddiv_rn(a.x, d), __ddiv_rn(a.y, d));
+}
+template <typename V> __device__ __forceinline__ V vzero();
+template <> __device__ __forceinline__ float4 vzero<float4>() {
+  return make_float4(0.f, 0.f, 0.f, 0.f);
+}
+template <> __device__ __forceinline__ double2 vzero<double2>() {
+  return make_double2(0.0, 0.0);
+}
+
+// 4 bf16 (8 bytes) -> float4, exact widening
+__device__ __forceinline__ float4 bf16x4_to_f4(uint2 raw) {
+  float4 r;
+  r.x = __uint_as_float(raw.x << 16);
+  r.y = __uint_as_float(raw.x & 0xffff0000u);
+  r.z = __uint_as_float(raw.y << 16);
+  r.w = __uint_as_float(raw.y & 0xffff0000u);
+  return r;
+}
+
+// load one accumulator-vector of input i from a generic (global or peer) address
+template <typename A>
+__device__ __forceinline__ typename VecT<A>::V ld_vec(const char *p,
+                                                      bool bf16) {
+  if constexpr (sizeof(A) == 4) {
+    if (bf16) {
+      uint2 raw;
+      asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                   : "=r"(raw.x), "=r"(raw.y)
+                   : "l"(p));
+      return bf16x4_to_f4(raw);
+    }
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+  } else {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p));
+    return v;
+  }
+}
+
+template <typename A>
+__device__ __forceinline__ typename VecT<A>::V lds_vec(const unsigned char *p,
+                                                       bool bf16) {
+  if constexpr (sizeof(A) == 4) {
+    if (bf16) return bf16x4_to_f4(*reinterpret_cast<const uint2 *>(p));
+    return *reinterpret_cast<const float4 *>(p);
+  } else {
+    return *reinterpret_cast<const double2 *>(p);
+  }
+}
+
+template <typename V> __device__ __forceinline__ void st_vec(char *p, const V &v) {
+  *reinterpret_cast<V *>(p) = v;
+}
+
+// Fixed-capacity register stack.  Indices are compared against the (warp-
+// uniform) stack pointer with fully unrolled predicates, so the array stays in
+// registers.
+template <int MAXD, typename V> struct Stack {
+  V s[MAXD];
+  int sp;
+  __device__ __forceinline__ Stack() : sp(0) {}
+  __device__ __forceinline__ void push(const V &v) {
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d)
+      if (d == sp) s[d] = v;
+    ++sp;
+  }
+  __device__ __forceinline__ void merge() {
+#pragma unroll
+    for (int d = 0; d + 1 < MAXD; ++d)
+      if (d + 2 == sp) s[d] = vadd(s[d], s[d + 1]);
+    --sp;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// kernel parameters
+
+struct FoldParams {
+  const char *in[RCV_MAX_IN];
+  char *out[RCV_MAX_OUT];
+  uint32_t smem_off[RCV_MAX_IN];  // TMA: byte offset of input i in a stage
+  uint8_t op[RCV_MAX_IN];
+  uint8_t bf16[RCV_MAX_IN];
+  int n_in;
+  int n_out;
+  unsigned long long nvec;  // accumulator vectors in this launch
+  double divisor;           // 0 => no scale
+  uint32_t stage_bytes;     // TMA
+  int stages;               // TMA
+  int vpt;                  // TMA: vectors per consumer thread per input
+};
+
+// ---------------------------------------------------------------------------
+// DIRECT variant
+
+template <typename A, int MAXD, int U>
+__global__ void __launch_bounds__(256)
+    fold_direct_kernel(const __grid_constant__ FoldParams p) {
+  using V = typename VecT<A>::V;
+  const unsigned long long nvec = p.nvec;
+  const unsigned long long step =
+      (unsigned long long)gridDim.x * blockDim.x * U;
+  for (unsigned long long chunk = (unsigned long long)blockIdx.x * blockDim.x * U;
+       chunk < nvec; chunk += step) {
+    const unsigned long long base = chunk + threadIdx.x;
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) ok[u] = base + (unsigned long long)u * blockDim.x < nvec;
+    Stack<MAXD, V> st[U];
+    V cur[U], nxt[U];
+    {
+      const bool b = p.bf16[0];
+      const int vb = b ? 8 : 16;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        cur[u] = ok[u] ? ld_vec<A>(p.in[0] + (base + (unsigned long long)u * blockDim.x) * vb, b)
+                       : vzero<V>();
+    }
+    for (int i = 0; i < p.n_in; ++i) {
+      if (i + 1 < p.n_in) {
+        const bool b = p.bf16[i + 1];
+        const int vb = b ? 8 : 16;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          nxt[u] = ok[u] ? ld_vec<A>(p.in[i + 1] + (base + (unsigned long long)u * blockDim.x) * vb, b)
+                         : vzero<V>();
+      }
+      const uint8_t op = p.op[i];
+      const int merges = op & RCV_OP_MERGES_MASK;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        st[u].push((op & RCV_OP_CANON) ? vcanon(cur[u]) : cur[u]);
+        for (int m = 0; m < merges; ++m) st[u].merge();
+        cur[u] = nxt[u];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!ok[u]) continue;
+      V r = st[u].s[0];
+      if (p.divisor != 0.0) r = vdiv(r, p.divisor);
+      const unsigned long long off = (base + (unsigned long long)u * blockDim.x) * 16ull;
+      for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + off, r);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA variant: cp.async.bulk producer warp + 4 consumer warps
+
+#define TMA_CONSUMERS 128
+#define TMA_THREADS (32 + TMA_CONSUMERS)
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile(
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+          smem_addr(bar)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src,
+                                         uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+template <typename A, int MAXD>
+__global__ void __launch_bounds__(TMA_THREADS)
+    fold_tma_kernel(const __grid_constant__ FoldParams p) {
+  using V = typename VecT<A>::V;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)p.stages * p.stage_bytes);
+  uint64_t *empty = full + p.stages;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], TMA_CONSUMERS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+
+  const unsigned long long tv = (unsigned long long)TMA_CONSUMERS * p.vpt;
+  const unsigned long long ntiles = (p.nvec + tv - 1) / tv;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t phase = 0;
+      for (unsigned long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        mbar_wait(&empty[s], phase ^ 1);
+        const unsigned long long v0 = t * tv;
+        const uint32_t nv = (uint32_t)min(tv, p.nvec - v0);
+        uint32_t total = 0;
+        for (int i = 0; i < p.n_in; ++i) total += nv * (p.bf16[i] ? 8u : 16u);
+        mbar_expect_tx(&full[s], total);
+        unsigned char *stage = smem + (size_t)s * p.stage_bytes;
+        for (int i = 0; i < p.n_in; ++i) {
+          const uint32_t vb = p.bf16[i] ? 8u : 16u;
+          bulk_g2s(stage + p.smem_off[i], p.in[i] + v0 * vb, nv * vb, &full[s]);
+        }
+        if (++s == p.stages) {
+          s = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+
+  const int ctid = threadIdx.x - 32;
+  int s = 0;
+  uint32_t phase = 0;
+  for (unsigned long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(&full[s], phase);
+    const unsigned long long v0 = t * tv;
+    const uint32_t nv = (uint32_t)min(tv, p.nvec - v0);
+    const unsigned char *stage = smem + (size_t)s * p.stage_bytes;
+    for (int u = 0; u < p.vpt; ++u) {
+      const uint32_t vi = (uint32_t)u * TMA_CONSUMERS + ctid;
+      if (vi >= nv) break;
+      Stack<MAXD, V> st;
+      for (int i = 0; i < p.n_in; ++i) {
+        const bool b = p.bf16[i];
+        V x = lds_vec<A>(stage + p.smem_off[i] + (size_t)vi * (b ? 8 : 16), b);
+        const uint8_t op = p.op[i];
+        st.push((op & RCV_OP_CANON) ? vcanon(x) : x);
+        const int merges = op & RCV_OP_MERGES_MASK;
+        for (int m = 0; m < merges; ++m) st.merge();
+      }
+      V r = st.s[0];
+      if (p.divisor != 0.0) r = vdiv(r, p.divisor);
+      const unsigned long long off = (v0 + vi) * 16ull;
+      for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + off, r);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == p.stages) {
+      s = 0;
+      phase ^= 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SCALAR variant (any alignment; heads, tails, misaligned views)
+
+struct ScalarParams {
+  const char *in[RCV_MAX_IN];
+  char *out[RCV_MAX_OUT];
+  uint8_t op[RCV_MAX_IN];
+  uint8_t bf16[RCV_MAX_IN];
+  int n_in;
+  int n_out;
+  unsigned long long numel;
+  double divisor;
+};
+
+template <typename A>
+__device__ __forceinline__ A ld_scalar(const char *base, unsigned long long e,
+                                       bool bf16) {
+  if constexpr (sizeof(A) == 4) {
+    if (bf16) {
+      const uint16_t raw = *reinterpret_cast<const uint16_t *>(base + e * 2);
+      return __uint_as_float(((uint32_t)raw) << 16);
+    }
+    return *reinterpret_cast<const float *>(base + e * 4);
+  } else {
+    return *reinterpret_cast<const double *>(base + e * 8);
+  }
+}
+__device__ __forceinline__ float sadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double sadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sdiv(float a, double d) { return __fdiv_rn(a, (float)d); }
+__device__ __forceinline__ double sdiv(double a, double d) { return __ddiv_rn(a, d); }
+
+template <typename A, int MAXD>
+__global__ void __launch_bounds__(256)
+    fold_scalar_kernel(const __grid_constant__ ScalarParams p) {
+  for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+       e < p.numel; e += (unsigned long long)gridDim.x * blockDim.x) {
+    A s[MAXD];
+    int sp = 0;
+    for (int i = 0; i < p.n_in; ++i) {
+      A x = ld_scalar<A>(p.in[i], e, p.bf16[i]);
+      if (p.op[i] & RCV_OP_CANON) x = sadd((A)0, x);
+#pragma unroll
+      for (int d = 0; d < MAXD; ++d)
+        if (d == sp) s[d] = x;
+      ++sp;
+      const int merges = p.op[i] & RCV_OP_MERGES_MASK;
+      for (int m = 0; m < merges; ++m) {
+#pragma unroll
+        for (int d = 0; d + 1 < MAXD; ++d)
+          if (d + 2 == sp) s[d] = sadd(s[d], s[d + 1]);
+        --sp;
+      }
+    }
+    A r = p.n_in ? s[0] : (A)0;
+    if (p.divisor != 0.0) r = sdiv(r, p.divisor);
+    for (int j = 0; j < p.n_out; ++j)
+      *reinterpret_cast<A *>(p.out[j] + e * sizeof(A)) = r;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// small utility kernels
+
+__global__ void compare_kernel(const uint32_t *a, const uint32_t *b,
+                               unsigned long long nwords,
+                               const uint8_t *ta, const uint8_t *tb, int ntail,
+                               unsigned long long *count) {
+  unsigned long long local = 0;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+       i < nwords; i += (unsigned long long)gridDim.x * blockDim.x)
+    local += (a[i] != b[i]);
+  if (blockIdx.x == 0 && threadIdx.x < ntail) local += (ta[threadIdx.x] != tb[threadIdx.x]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, local);
+}
+
+template <typename T>
+__global__ void sgd_kernel(T *params, const T *flat, unsigned long long n,
+                           double b, double lr) {
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+       i < n; i += (unsigned long long)gridDim.x * blockDim.x) {
+    if constexpr (sizeof(T) == 8) {
+      params[i] = __dsub_rn(params[i], __dmul_rn(lr, __ddiv_rn(flat[i], b)));
+    } else {
+      params[i] = __fsub_rn(params[i],
+                            __fmul_rn((float)lr, __fdiv_rn(flat[i], (float)b)));
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void unit_lanes_kernel(double *out, uint64_t base,
+                                  unsigned long long n, double scale,
+                                  double shift, int floor7) {
+  for (unsigned long long l = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+       l < n; l += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint64_t z = mix64(base + (uint64_t)l * 0x9E3779B97F4A7C15ull);
+    double u = __dmul_rn(__ull2double_rn(z >> 11), 0x1.0p-53);
+    // numpy evaluates `u * scale + shift` as two roundings
+    u = __dadd_rn(__dmul_rn(u, scale), shift);
+    if (floor7) u = __dsub_rn(floor(__dmul_rn(u, 7.0)), 3.0);
+    out[l] = u;
+  }
+}
+
+// Fixed-order dot products: TOY_T threads each fold a contiguous chunk in
+// index order, then thread 0 folds the chunk sums in thread order.
+#define TOY_T 256
+__global__ void toy_dot_kernel(int linear, const double *params,
+                               const double *lanes, const double *wstar,
+                               unsigned long long dim, double *scal) {
+  __shared__ double part_p[TOY_T], part_w[TOY_T];
+  const unsigned long long chunk = (dim + TOY_T - 1) / TOY_T;
+  const unsigned long long lo = threadIdx.x * chunk;
+  const unsigned long long hi = min(dim, lo + chunk);
+  double sp = 0.0, sw = 0.0;
+  for (unsigned long long i = lo; i < hi; ++i) {
+    sp = __dadd_rn(sp, __dmul_rn(params[i], lanes[i]));
+    if (linear) sw = __dadd_rn(sw, __dmul_rn(wstar[i], lanes[i]));
+  }
+  part_p[threadIdx.x] = sp;
+  part_w[threadIdx.x] = sw;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tp = 0.0, tw = 0.0;
+    for (int t = 0; t < TOY_T; ++t) {
+      tp = __dadd_rn(tp, part_p[t]);
+      tw = __dadd_rn(tw, part_w[t]);
+    }
+    if (linear) {
+      const double y = __dadd_rn(tw, __dmul_rn(0.1, lanes[dim]));
+      const double r = __dsub_rn(tp, y);
+      scal[0] = r;               // residual
+      scal[1] = __dmul_rn(r, r); // loss
+    } else {
+      scal[0] = 1.0;
+      scal[1] = tp;
+    }
+  }
+}
+
+__global__ void toy_grad_kernel(int linear, const double *lanes,
+                                unsigned long long dim, const double *scal,
+                                double *grad) {
+  const double r = scal[0];
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+       i < dim; i += (unsigned long long)gridDim.x * blockDim.x)
+    grad[i] = linear ? __dmul_rn(r, lanes[i]) : lanes[i];
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+namespace {
+
+struct DevInfo {
+  int sms = 0;
+  bool tma_attr_set[3][4] = {};
+};
+std::mutex g_mu;
+std::vector<DevInfo> g_dev;
+
+int dev_sms(int dev) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if ((int)g_dev.size() <= dev) g_dev.resize(dev + 1);
+  if (!g_dev[dev].sms) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    g_dev[dev].sms = v;
+  }
+  return g_dev[dev].sms;
+}
+
+int esize(int dt) { return dt == RCV_F64 ? 8 : (dt == RCV_F32 ? 4 : 2); }
+
+struct FoldReq {
+  int n_in = 0;
+  const char *in[RCV_MAX_IN];
+  int in_dt[RCV_MAX_IN];
+  uint8_t op[RCV_MAX_IN];
+  int n_out = 0;
+  char *out[RCV_MAX_OUT];
+  int acc_dt = RCV_F32;
+  double divisor = 0.0;
+};
+
+// simulate the program on the host: validates it and returns the max depth
+int program_depth(const uint8_t *ops, int n, int *max_depth) {
+  int sp = 0, mx = 0;
+  for (int i = 0; i < n; ++i) {
+    ++sp;
+    mx = std::max(mx, sp);
+    const int m = ops[i] & RCV_OP_MERGES_MASK;
+    if (m > sp - 1) return set_err(RCV_EINVAL, "fold program: input %d merges %d with stack depth %d", i, m, sp);
+    sp -= m;
+  }
+  if (n > 0 && sp != 1)
+    return set_err(RCV_EINVAL, "fold program leaves %d values on the stack (want 1)", sp);
+  *max_depth = mx;
+  return RCV_OK;
+}
+
+template <typename A, int MAXD>
+int launch_scalar_t(const FoldReq &r, unsigned long long e0, unsigned long long n,
+                    cudaStream_t st, int sms) {
+  ScalarParams p;
+  memset(&p, 0, sizeof p);
+  p.n_in = r.n_in;
+  p.n_out = r.n_out;
+  for (int i = 0; i < r.n_in; ++i) {
+    p.in[i] = r.in[i] + e0 * esize(r.in_dt[i]);
+    p.op[i] = r.op[i];
+    p.bf16[i] = r.in_dt[i] == RCV_BF16;
+  }
+  for (int j = 0; j < r.n_out; ++j) p.out[j] = r.out[j] + e0 * sizeof(A);
+  p.numel = n;
+  p.divisor = r.divisor;
+  const unsigned long long blocks = std::min<unsigned long long>((n + 255) / 256, (unsigned long long)sms * 8);
+  fold_scalar_kernel<A, MAXD><<<(unsigned)std::max<unsigned long long>(blocks, 1), 256, 0, st>>>(p);
+  CK(cudaGetLastError());
+  return RCV_OK;
+}
+
+template <typename A>
+int launch_scalar(const FoldReq &r, int maxd, unsigned long long e0, unsigned long long n,
+                  cudaStream_t st, int sms) {
+  if (n == 0) return RCV_OK;
+  if (maxd <= 2) return launch_scalar_t<A, 2>(r, e0, n, st, sms);
+  if (maxd <= 4) return launch_scalar_t<A, 4>(r, e0, n, st, sms);
+  if (maxd <= 8) return launch_scalar_t<A, 8>(r, e0, n, st, sms);
+  return set_err(RCV_ERANGE, "fold program stack depth %d exceeds 8", maxd);
+}
+
+template <typename A>
+void fill_vec_params(FoldParams &p, const FoldReq &r, unsigned long long e0,
+                     unsigned long long nvec) {
+  memset(&p, 0, sizeof p);
+  p.n_in = r.n_in;
+  p.n_out = r.n_out;
+  for (int i = 0; i < r.n_in; ++i) {
+    p.in[i] = r.in[i] + e0 * esize(r.in_dt[i]);
+    p.op[i] = r.op[i];
+    p.bf16[i] = r.in_dt[i] == RCV_BF16;
+  }
+  for (int j = 0; j < r.n_out; ++j) p.out[j] = r.out[j] + e0 * sizeof(A);
+  p.nvec = nvec;
+  p.divisor = r.divisor;
+}
+
+template <typename A, int MAXD>
+int launch_direct_t(const FoldReq &r, unsigned long long e0, unsigned long long nvec,
+                    cudaStream_t st, int sms) {
+  FoldParams p;
+  fill_vec_params<A>(p, r, e0, nvec);
+  constexpr int U = MAXD <= 2 ? 4 : (MAXD <= 4 ? 2 : 1);
+  const unsigned long long per_block = 256ull * U;
+  const unsigned long long want = (nvec + per_block - 1) / per_block;
+  const unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)sms * 8));
+  fold_direct_kernel<A, MAXD, U><<<(unsigned)blocks, 256, 0, st>>>(p);
+  CK(cudaGetLastError());
+  return RCV_OK;
+}
+
+template <typename A>
+int launch_direct(const FoldReq &r, int maxd, unsigned long long e0, unsigned long long nvec,
+                  cudaStream_t st, int sms) {
+  if (maxd <= 2) return launch_direct_t<A, 2>(r, e0, nvec, st, sms);
+  if (maxd <= 4) return launch_direct_t<A, 4>(r, e0, nvec, st, sms);
+  if (maxd <= 8) return launch_direct_t<A, 8>(r, e0, nvec, st, sms);
+  return set_err(RCV_ERANGE, "fold program stack depth %d exceeds 8", maxd);
+}
+
+// TMA geometry: vectors-per-thread, stages, CTAs per SM
+struct TmaGeom {
+  int vpt, stages, ctas_per_sm;
+  uint32_t stage_bytes;
+  size_t smem;
+};
+
+bool tma_geom(const FoldReq &r, TmaGeom *g) {
+  uint32_t bytes_per_vec = 0;  // sum over inputs of one vector
+  for (int i = 0; i < r.n_in; ++i) bytes_per_vec += r.in_dt[i] == RCV_BF16 ? 8 : 16;
+  const uint32_t per_vpt = bytes_per_vec * TMA_CONSUMERS;  // stage bytes at vpt=1
+  int vpt = 1;
+  while (vpt < 8 && per_vpt * (vpt * 2) <= 32768) vpt *= 2;
+  const uint32_t stage = per_vpt * vpt;
+  const size_t budget2 = 100 * 1024, budget1 = 200 * 1024;
+  int ctas = 2, stages = (int)std::min<size_t>(8, budget2 / stage);
+  if (stages < 3) {
+    ctas = 1;
+    stages = (int)std::min<size_t>(8, budget1 / stage);
+  }
+  if (stages < 2) return false;
+  g->vpt = vpt;
+  g->stages = stages;
+  g->ctas_per_sm = ctas;
+  g->stage_bytes = stage;
+  g->smem = (size_t)stages * stage + 2 * stages * sizeof(uint64_t);
+  return true;
+}
+
+template <typename A, int MAXD>
+int launch_tma_t(const FoldReq &r, const TmaGeom &g, unsigned long long e0,
+                 unsigned long long nvec, cudaStream_t st, int sms) {
+  FoldParams p;
+  fill_vec_params<A>(p, r, e0, nvec);
+  uint32_t off = 0;
+  for (int i = 0; i < r.n_in; ++i) {
+    p.smem_off[i] = off;
+    off += (uint32_t)TMA_CONSUMERS * g.vpt * (p.bf16[i] ? 8u : 16u);
+  }
+  p.stage_bytes = g.stage_bytes;
+  p.stages = g.stages;
+  p.vpt = g.vpt;
+  auto kern = fold_tma_kernel<A, MAXD>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+  const unsigned long long tv = (unsigned long long)TMA_CONSUMERS * g.vpt;
+  const unsigned long long ntiles = (nvec + tv - 1) / tv;
+  const unsigned long long blocks = std::max<unsigned long long>(
+      1, std::min<unsigned long long>(ntiles, (unsigned long long)sms * g.ctas_per_sm));
+  kern<<<(unsigned)blocks, TMA_THREADS, g.smem, st>>>(p);
+  CK(cudaGetLastError());
+  return RCV_OK;
+}
+
+template <typename A>
+int launch_tma(const FoldReq &r, const TmaGeom &g, int maxd, unsigned long long e0,
+               unsigned long long nvec, cudaStream_t st, int sms) {
+  if (maxd <= 2) return launch_tma_t<A, 2>(r, g, e0, nvec, st, sms);
+  if (maxd <= 4) return launch_tma_t<A, 4>(r, g, e0, nvec, st, sms);
+  if (maxd <= 8) return launch_tma_t<A, 8>(r, g, e0, nvec, st, sms);
+  return set_err(RCV_ERANGE, "fold program stack depth %d exceeds 8", maxd);
+}
+
+// head elements h (< 8) after which every pointer is 16-byte aligned, or -1
+int common_head(const FoldReq &r) {
+  for (int h = 0; h < 8; ++h) {
+    bool ok = true;
+    for (int i = 0; i < r.n_in && ok; ++i)
+      ok = ((uintptr_t)(r.in[i] + (size_t)h * esize(r.in_dt[i])) & 15) == 0;
+    for (int j = 0; j < r.n_out && ok; ++j)
+      ok = ((uintptr_t)(r.out[j] + (size_t)h * esize(r.acc_dt)) & 15) == 0;
+    if (ok) return h;
+  }
+  return -1;
+}
+
+int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int sms) {
+  if (numel == 0 || r.n_out == 0) return RCV_OK;
+  int maxd = 1;
+  int rc = program_depth(r.op, r.n_in, &maxd);
+  if (rc) return rc;
+  if (r.n_in == 0) {
+    for (int j = 0; j < r.n_out; ++j) CK(cudaMemsetAsync(r.out[j], 0, numel * esize(r.acc_dt), st));
+    return RCV_OK;
+  }
+  const bool f64 = r.acc_dt == RCV_F64;
+  const int E = f64 ? 2 : 4;
+  int h = variant == RCV_VARIANT_SCALAR ? -1 : common_head(r);
+  if (h < 0 || (size_t)h >= numel) {
+    return f64 ? launch_scalar<double>(r, maxd, 0, numel, st, sms)
+               : launch_scalar<float>(r, maxd, 0, numel, st, sms);
+  }
+  unsigned long long nvec = (numel - h) / E;
+  nvec &= ~1ull;  // even: bf16 inputs then move whole 16-byte units
+  const unsigned long long body_end = h + nvec * E;
+  if (h) {
+    rc = f64 ? launch_scalar<double>(r, maxd, 0, h, st, sms) : launch_scalar<float>(r, maxd, 0, h, st, sms);
+    if (rc) return rc;
+  }
+  if (nvec) {
+    TmaGeom g;
+    bool use_tma = variant == RCV_VARIANT_TMA || variant == RCV_VARIANT_AUTO;
+    if (use_tma && !tma_geom(r, &g)) {
+      if (variant == RCV_VARIANT_TMA)
+        return set_err(RCV_EINVAL, "TMA variant: %d inputs do not fit a 2-stage ring", r.n_in);
+      use_tma = false;
+    }
+    if (use_tma)
+      rc = f64 ? launch_tma<double>(r, g, maxd, h, nvec, st, sms) : launch_tma<float>(r, g, maxd, h, nvec, st, sms);
+    else
+      rc = f64 ? launch_direct<double>(r, maxd, h, nvec, st, sms) : launch_direct<float>(r, maxd, h, nvec, st, sms);
+    if (rc) return rc;
+  }
+  if (body_end < numel) {
+    rc = f64 ? launch_scalar<double>(r, maxd, body_end, numel - body_end, st, sms)
+             : launch_scalar<float>(r, maxd, body_end, numel - body_end, st, sms);
+    if (rc) return rc;
+  }
+  return RCV_OK;
+}
+
+int check_dtype(int acc_dt, int in_dt) {
+  if (acc_dt != RCV_F32 && acc_dt != RCV_F64) return set_err(RCV_EINVAL, "acc dtype %d must be F32 or F64", acc_dt);
+  if (in_dt == acc_dt) return RCV_OK;
+  if (in_dt == RCV_BF16 && acc_dt == RCV_F32) return RCV_OK;
+  return set_err(RCV_EINVAL, "input dtype %d cannot feed accumulator dtype %d", in_dt, acc_dt);
+}
+
+int current_device_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev_sms(dev);
+}
+
+// post-order emission of the canonical tree
+struct TreeBuild {
+  const uint32_t *lo, *level;
+  int n, cur;
+  uint8_t *ops;
+  int depth, max_depth;
+  int last_push;
+  int err;
+  bool emit(uint32_t lev, uint64_t idx) {
+    const uint64_t a = idx << lev, b = a + (1ull << lev);
+    if (cur >= n || lo[cur] >= b) return false;
+    if (lo[cur] == a && level[cur] == lev) {
+      ops[cur] = 0;
+      last_push = cur++;
+      if (++depth > max_depth) max_depth = depth;
+      return true;
+    }
+    if (lev == 0) {
+      err = 1;
+      return false;
+    }
+    const bool l = emit(lev - 1, 2 * idx);
+    const bool rr = emit(lev - 1, 2 * idx + 1);
+    if (l && rr) {
+      ops[last_push] += 1;
+      --depth;
+    }
+    return l || rr;
+  }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+const char *rcv_last_error(void) { return g_err.c_str(); }
+int rcv_version(void) { return RCV_VERSION; }
+
+int rcv_device_count(int *n) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  *n = c;
+  return RCV_OK;
+}
+
+int rcv_enable_peer_access(int n_dev, const int *devices) {
+  int prev = 0;
+  CK(cudaGetDevice(&prev));
+  for (int a = 0; a < n_dev; ++a) {
+    for (int b = 0; b < n_dev; ++b) {
+      if (a == b) continue;
+      int can = 0;
+      CK(cudaDeviceCanAccessPeer(&can, devices[a], devices[b]));
+      if (!can) return set_err(RCV_EINVAL, "device %d cannot access peer %d", devices[a], devices[b]);
+      CK(cudaSetDevice(devices[a]));
+      cudaError_t e = cudaDeviceEnablePeerAccess(devices[b], 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else if (e != cudaSuccess) {
+        return set_err(RCV_ECUDA, "enable peer %d->%d: %s", devices[a], devices[b], cudaGetErrorString(e));
+      }
+    }
+  }
+  CK(cudaSetDevice(prev));
+  return RCV_OK;
+}
+
+int rcv_fold(int n_in, const void *const *in, const uint8_t *ops,
+             const int *in_dtypes, int n_out, void *const *out, int acc_dtype,
+             size_t numel, double divisor, int variant, void *stream) {
+  if (n_in < 0 || n_in > RCV_MAX_IN || n_out < 0 || n_out > RCV_MAX_OUT)
+    return set_err(RCV_ERANGE, "n_in %d / n_out %d out of range", n_in, n_out);
+  FoldReq r;
+  r.n_in = n_in;
+  r.n_out = n_out;
+  r.acc_dt = acc_dtype;
+  r.divisor = divisor;
+  for (int i = 0; i < n_in; ++i) {
+    int rc = check_dtype(acc_dtype, in_dtypes[i]);
+    if (rc) return rc;
+    r.in[i] = (const char *)in[i];
+    r.in_dt[i] = in_dtypes[i];
+    r.op[i] = ops[i];
+  }
+  if (acc_dtype != RCV_F32 && acc_dtype != RCV_F64) return check_dtype(acc_dtype, acc_dtype);
+  for (int j = 0; j < n_out; ++j) r.out[j] = (char *)out[j];
+  return run_fold(r, numel, variant, (cudaStream_t)stream, current_device_sms());
+}
+
+static int build_allreduce(FoldReq &r, void *const *views, int n, uint64_t contrib_mask,
+                           int dtype, double divisor) {
+  if (n < 1 || n > RCV_MAX_OUT) return set_err(RCV_ERANGE, "member count %d out of range", n);
+  if (n < 64 && (contrib_mask >> n)) return set_err(RCV_EINVAL, "contributor mask names non-members");
+  int rc = check_dtype(dtype, dtype);
+  if (rc) return rc;
+  r.acc_dt = dtype;
+  r.divisor = divisor;
+  r.n_in = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!((contrib_mask >> i) & 1)) continue;
+    r.in[r.n_in] = (const char *)views[i];
+    r.in_dt[r.n_in] = dtype;
+    r.op[r.n_in] = r.n_in ? 1 : 0;  // first contributor is copied, later ones added
+    ++r.n_in;
+  }
+  r.n_out = n;
+  for (int i = 0; i < n; ++i) r.out[i] = (char *)views[i];
+  return RCV_OK;
+}
+
+int rcv_masked_allreduce(void *const *views, int n, uint64_t contrib_mask,
+                         int dtype, size_t numel, double divisor,
+                         void *stream) {
+  FoldReq r;
+  int rc = build_allreduce(r, views, n, contrib_mask, dtype, divisor);
+  if (rc) return rc;
+  return run_fold(r, numel, RCV_VARIANT_AUTO, (cudaStream_t)stream, current_device_sms());
+}
+
+int rcv_masked_allreduce_multidev(void *const *views, int n,
+                                  uint64_t contrib_mask, int dtype,
+                                  size_t numel, double divisor, int n_dev,
+                                  const int *devices, void *const *streams) {
+  if (n_dev < 1 || n_dev > 64) return set_err(RCV_ERANGE, "device count %d out of range", n_dev);
+  FoldReq r;
+  int rc = build_allreduce(r, views, n, contrib_mask, dtype, divisor);
+  if (rc) return rc;
+  if (numel == 0) return RCV_OK;
+  int prev = 0;
+  CK(cudaGetDevice(&prev));
+  // entry: every device's stream waits for every other stream's prior work
+  // (the contributors' accumulation), exit: likewise for the peers' stores.
+  std::vector<cudaEvent_t> ev(n_dev);
+  auto cross_order = [&]() -> int {
+    for (int d = 0; d < n_dev; ++d) {
+      CK(cudaSetDevice(devices[d]));
+      CK(cudaEventCreateWithFlags(&ev[d], cudaEventDisableTiming));
+      CK(cudaEventRecord(ev[d], (cudaStream_t)streams[d]));
+    }
+    for (int d = 0; d < n_dev; ++d) {
+      CK(cudaSetDevice(devices[d]));
+      for (int o = 0; o < n_dev; ++o)
+        if (o != d) CK(cudaStreamWaitEvent((cudaStream_t)streams[d], ev[o], 0));
+    }
+    for (int d = 0; d < n_dev; ++d) CK(cudaEventDestroy(ev[d]));
+    return RCV_OK;
+  };
+  rc = cross_order();
+  if (rc) return rc;
+  // owner slices, multiples of 8 elements (16-byte units for f32/f64 and bf16)
+  const size_t unit = 8;
+  const size_t units = (numel + unit - 1) / unit;
+  for (int d = 0; d < n_dev; ++d) {
+    const size_t a = std::min(numel, units * d / n_dev * unit);
+    const size_t b = std::min(numel, units * (d + 1) / n_dev * unit);
+    if (b <= a) continue;
+    CK(cudaSetDevice(devices[d]));
+    FoldReq s = r;
+    const int es = esize(dtype);
+    for (int i = 0; i < s.n_in; ++i) s.in[i] += a * es;
+    for (int j = 0; j < s.n_out; ++j) s.out[j] += a * es;
+    rc = run_fold(s, b - a, RCV_VARIANT_AUTO, (cudaStream_t)streams[d], dev_sms(devices[d]));
+    if (rc) return rc;
+  }
+  rc = cross_order();
+  if (rc) return rc;
+  CK(cudaSetDevice(prev));
+  return RCV_OK;
+}
+
+int rcv_accumulate(void *acc, const void *grad, int acc_dtype, int grad_dtype,
+                   size_t numel, int first, void *stream) {
+  int rc = check_dtype(acc_dtype, grad_dtype);
+  if (rc) return rc;
+  FoldReq r;
+  r.acc_dt = acc_dtype;
+  if (first) {
+    r.n_in = 1;
+    r.in[0] = (const char *)grad;
+    r.in_dt[0] = grad_dtype;
+    r.op[0] = RCV_OP_CANON;
+  } else {
+    r.n_in = 2;
+    r.in[0] = (const char *)acc;
+    r.in_dt[0] = acc_dtype;
+    r.op[0] = 0;
+    r.in[1] = (const char *)grad;
+    r.in_dt[1] = grad_dtype;
+    r.op[1] = 1;
+  }
+  r.n_out = 1;
+  r.out[0] = (char *)acc;
+  return run_fold(r, numel, RCV_VARIANT_AUTO, (cudaStream_t)stream, current_device_sms());
+}
+
+int rcv_tree_program(const uint32_t *lo, const uint32_t *level, int n_blocks,
+                     uint32_t n_leaves, uint8_t *ops_out, int *max_depth) {
+  if (n_blocks < 0 || n_blocks > RCV_MAX_IN) return set_err(RCV_ERANGE, "block count %d out of range", n_blocks);
+  if (n_leaves < 1) return set_err(RCV_EINVAL, "n_leaves must be >= 1");
+  uint32_t L = 0;
+  while ((1ull << L) < n_leaves) ++L;
+  for (int i = 0; i < n_blocks; ++i) {
+    if (level[i] > L) return set_err(RCV_EINVAL, "block %d level %u above tree height %u", i, level[i], L);
+    const uint64_t sz = 1ull << level[i];
+    if (lo[i] % sz) return set_err(RCV_EINVAL, "block %d (lo %u, level %u) is not aligned", i, lo[i], level[i]);
+    if ((uint64_t)lo[i] + sz > (1ull << L)) return set_err(RCV_EINVAL, "block %d exceeds the tree", i);
+    if (i && (uint64_t)lo[i - 1] + (1ull << level[i - 1]) > lo[i])
+      return set_err(RCV_EINVAL, "blocks %d and %d overlap or are unsorted", i - 1, i);
+  }
+  TreeBuild tb{lo, level, n_blocks, 0, ops_out, 0, 0, -1, 0};
+  if (n_blocks) tb.emit(L, 0);
+  if (tb.err || tb.cur != n_blocks) return set_err(RCV_EINVAL, "blocks do not form a canonical tree cover");
+  *max_depth = tb.max_depth;
+  return RCV_OK;
+}
+
+int rcv_tree_commit(const rcv_block *blocks, int n_blocks, uint32_t n_leaves,
+                    int n_out, void *const *out, int acc_dtype, size_t numel,
+                    double divisor, int variant, void *stream) {
+  if (n_blocks < 0 || n_blocks > RCV_MAX_IN || n_out < 0 || n_out > RCV_MAX_OUT)
+    return set_err(RCV_ERANGE, "block/output count out of range");
+  uint32_t lo[RCV_MAX_IN], lev[RCV_MAX_IN];
+  for (int i = 0; i < n_blocks; ++i) {
+    lo[i] = blocks[i].lo;
+    lev[i] = blocks[i].level;
+  }
+  FoldReq r;
+  int depth = 0;
+  int rc = rcv_tree_program(lo, lev, n_blocks, n_leaves, r.op, &depth);
+  if (rc) return rc;
+  r.n_in = n_blocks;
+  r.acc_dt = acc_dtype;
+  r.divisor = divisor;
+  for (int i = 0; i < n_blocks; ++i) {
+    rc = check_dtype(acc_dtype, blocks[i].dtype);
+    if (rc) return rc;
+    r.in[i] = (const char *)blocks[i].ptr;
+    r.in_dt[i] = blocks[i].dtype;
+  }
+  r.n_out = n_out;
+  for (int j = 0; j < n_out; ++j) r.out[j] = (char *)out[j];
+  return run_fold(r, numel, variant, (cudaStream_t)stream, current_device_sms());
+}
+
+int rcv_copy(void *dst, const void *src, size_t bytes, void *stream) {
+  if (!bytes || dst == src) return RCV_OK;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return RCV_OK;
+}
+
+int rcv_zero(void *dst, size_t bytes, void *stream) {
+  if (!bytes) return RCV_OK;
+  CK(cudaMemsetAsync(dst, 0, bytes, (cudaStream_t)stream));
+  return RCV_OK;
+}
+
+int rcv_compare(const void *a, const void *b, size_t bytes,
+                unsigned long long *d_count, void *stream) {
+  if (!bytes) return RCV_OK;
+  const unsigned long long nw = bytes / 4;
+  const int tail = (int)(bytes % 4);
+  const int sms = current_device_sms();
+  const unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>((nw + 255) / 256, (unsigned long long)sms * 8));
+  compare_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+      (const uint32_t *)a, (const uint32_t *)b, nw, (const uint8_t *)a + nw * 4,
+      (const uint8_t *)b + nw * 4, tail, d_count);
+  CK(cudaGetLastError());
+  return RCV_OK;
+}
+
+int rcv_sgd_commit(void *params, const void *flat, int dtype, size_t numel,
+                   double b, double lr, void *stream) {
+  if (!numel) return RCV_OK;
+  const int sms = current_device_sms();
+  const unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>((numel + 255) / 256, (unsigned long long)sms * 8));
+  if (dtype == RCV_F64)
+    sgd_kernel<double><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>((double *)params, (const double *)flat, numel, b, lr);
+  else if (dtype == RCV_F32)
+    sgd_kernel<float><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>((float *)params, (const float *)flat, numel, b, lr);
+  else
+    return set_err(RCV_EINVAL, "sgd dtype %d", dtype);
+  CK(cudaGetLastError());
+  return RCV_OK;
+}
+
+int rcv_unit_lanes(double *out, uint64_t base, size_t n, double scale,
+                   double shift, int floor7, void *stream) {
+  if (!n) return RCV_OK;
+  const int sms = current_device_sms();
+  const unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>((n + 255) / 256, (unsigned long long)sms * 8));
+  unit_lanes_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(out, base, n, scale, shift, floor7);
+  CK(cudaGetLastError());
+  return RCV_OK;
+}
+
+int rcv_toy_grad(int kind_linear, const double *params, const double *lanes,
+                 const double *wstar, size_t dim, double *grad, double *scal,
+                 void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  toy_dot_kernel<<<1, TOY_T, 0, st>>>(kind_linear, params, lanes, wstar, dim, scal);
+  CK(cudaGetLastError());
+  if (dim && grad) {  // grad == NULL: loss only (the constant stream's x is g0)
+    const int sms = current_device_sms();
+    const unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>((dim + 255) / 256, (unsigned long long)sms * 8));
+    toy_grad_kernel<<<(unsigned)blocks, 256, 0, st>>>(kind_linear, lanes, dim, scal, grad);
+    CK(cudaGetLastError());
+  }
+  return RCV_OK;
+}
+
+}  // extern "C"
