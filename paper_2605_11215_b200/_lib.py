@@ -295,11 +295,12 @@ def unit_lanes(out: torch.Tensor, base: int, scale: float = 1.0,
 def toy_grad(linear: bool, params: torch.Tensor, lanes: torch.Tensor,
              wstar: Optional[torch.Tensor], grad: torch.Tensor,
              scal: torch.Tensor) -> None:
-    for t in (params, lanes, grad, scal):
+    for t in (params, lanes, scal) + ((grad,) if grad is not None else ()):
         require_cuda(t)
     dim = params.numel()
     _check(load().rcv_toy_grad(int(linear), params.data_ptr(),
                                lanes.data_ptr(),
                                wstar.data_ptr() if wstar is not None else None,
-                               dim, grad.data_ptr(), scal.data_ptr(),
+                               dim, grad.data_ptr() if grad is not None else None,
+                               scal.data_ptr(),
                                stream_of(grad)))

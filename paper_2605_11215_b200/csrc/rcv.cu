@@ -194,60 +194,89 @@ struct FoldParams {
   uint32_t stage_bytes;     // TMA
   int stages;               // TMA
   int vpt;                  // TMA: vectors per consumer thread per input
+  // canonical tree (ProgTree): heap-indexed nodes, id = 2^(L-level)-1+idx
+  int8_t node_in[2 * RCV_MAX_IN - 1];    // input feeding the node, or -1
+  uint8_t present[2 * RCV_MAX_IN - 1];   // subtree holds at least one input
 };
 
 // ---------------------------------------------------------------------------
-// DIRECT variant
+// fold programs: evaluate one accumulator-vector from a loader ld(i) -> V.
+// All control flow below depends only on kernel parameters, so it is uniform
+// across the grid; no thread ever diverges.
 
-template <typename A, int MAXD, int U>
+// Generic: the stack program of include/rcv.h (push; merge top two).
+template <int MAXD> struct ProgStack {
+  template <typename V, typename Ld>
+  __device__ __forceinline__ static V eval(const FoldParams &p, const Ld &ld) {
+    Stack<MAXD, V> st;
+    for (int i = 0; i < p.n_in; ++i) {
+      V x = ld(i);
+      const uint8_t op = p.op[i];
+      st.push((op & RCV_OP_CANON) ? vcanon(x) : x);
+      const int merges = op & RCV_OP_MERGES_MASK;
+      for (int m = 0; m < merges; ++m) st.merge();
+    }
+    return st.s[0];
+  }
+};
+
+// Left fold ((x0 + x1) + x2) + ...: the reference collective's order
+// (comm.py:192-196) and the accumulation `flat += grad` (trainer.py:212).
+struct ProgLeft {
+  template <typename V, typename Ld>
+  __device__ __forceinline__ static V eval(const FoldParams &p, const Ld &ld) {
+    V acc = ld(0);
+    if (p.op[0] & RCV_OP_CANON) acc = vcanon(acc);
+    for (int i = 1; i < p.n_in; ++i) acc = vadd(acc, ld(i));
+    return acc;
+  }
+};
+
+// Canonical dyadic tree of height L, unrolled at compile time: a node is its
+// input when one feeds it, else left + right when both subtrees hold
+// something, else the non-empty side (empty leaves are skipped, not zeros).
+template <int L> struct ProgTree {
+  template <int LEVEL, int IDX, typename V, typename Ld>
+  __device__ __forceinline__ static bool node(const FoldParams &p, const Ld &ld, V &out) {
+    constexpr int id = (1 << (L - LEVEL)) - 1 + IDX;
+    if (!p.present[id]) return false;
+    const int in = p.node_in[id];
+    if (in >= 0) {
+      out = ld(in);
+      return true;
+    }
+    if constexpr (LEVEL > 0) {
+      V a = vzero<V>(), b = vzero<V>();
+      const bool pa = node<LEVEL - 1, 2 * IDX>(p, ld, a);
+      const bool pb = node<LEVEL - 1, 2 * IDX + 1>(p, ld, b);
+      out = pa ? (pb ? vadd(a, b) : a) : b;
+    }
+    return true;
+  }
+  template <typename V, typename Ld>
+  __device__ __forceinline__ static V eval(const FoldParams &p, const Ld &ld) {
+    V r = vzero<V>();
+    node<L, 0>(p, ld, r);
+    return r;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// DIRECT variant: 128-bit LDG straight from (local or peer) global memory
+
+template <typename A, typename Prog>
 __global__ void __launch_bounds__(256)
     fold_direct_kernel(const __grid_constant__ FoldParams p) {
   using V = typename VecT<A>::V;
-  const unsigned long long nvec = p.nvec;
-  const unsigned long long step =
-      (unsigned long long)gridDim.x * blockDim.x * U;
-  for (unsigned long long chunk = (unsigned long long)blockIdx.x * blockDim.x * U;
-       chunk < nvec; chunk += step) {
-    const unsigned long long base = chunk + threadIdx.x;
-    bool ok[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) ok[u] = base + (unsigned long long)u * blockDim.x < nvec;
-    Stack<MAXD, V> st[U];
-    V cur[U], nxt[U];
-    {
-      const bool b = p.bf16[0];
-      const int vb = b ? 8 : 16;
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        cur[u] = ok[u] ? ld_vec<A>(p.in[0] + (base + (unsigned long long)u * blockDim.x) * vb, b)
-                       : vzero<V>();
-    }
-    for (int i = 0; i < p.n_in; ++i) {
-      if (i + 1 < p.n_in) {
-        const bool b = p.bf16[i + 1];
-        const int vb = b ? 8 : 16;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          nxt[u] = ok[u] ? ld_vec<A>(p.in[i + 1] + (base + (unsigned long long)u * blockDim.x) * vb, b)
-                         : vzero<V>();
-      }
-      const uint8_t op = p.op[i];
-      const int merges = op & RCV_OP_MERGES_MASK;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        st[u].push((op & RCV_OP_CANON) ? vcanon(cur[u]) : cur[u]);
-        for (int m = 0; m < merges; ++m) st[u].merge();
-        cur[u] = nxt[u];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (!ok[u]) continue;
-      V r = st[u].s[0];
-      if (p.divisor != 0.0) r = vdiv(r, p.divisor);
-      const unsigned long long off = (base + (unsigned long long)u * blockDim.x) * 16ull;
-      for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + off, r);
-    }
+  for (unsigned long long v = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+       v < p.nvec; v += (unsigned long long)gridDim.x * blockDim.x) {
+    auto ld = [&](int i) {
+      const bool b = p.bf16[i];
+      return ld_vec<A>(p.in[i] + v * (b ? 8ull : 16ull), b);
+    };
+    V r = Prog::template eval<V>(p, ld);
+    if (p.divisor != 0.0) r = vdiv(r, p.divisor);
+    for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + v * 16ull, r);
   }
 }
 
@@ -296,7 +325,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src,
       : "memory");
 }
 
-template <typename A, int MAXD>
+template <typename A, typename Prog>
 __global__ void __launch_bounds__(TMA_THREADS)
     fold_tma_kernel(const __grid_constant__ FoldParams p) {
   using V = typename VecT<A>::V;
@@ -354,16 +383,11 @@ __global__ void __launch_bounds__(TMA_THREADS)
     for (int u = 0; u < p.vpt; ++u) {
       const uint32_t vi = (uint32_t)u * TMA_CONSUMERS + ctid;
       if (vi >= nv) break;
-      Stack<MAXD, V> st;
-      for (int i = 0; i < p.n_in; ++i) {
+      auto ld = [&](int i) {
         const bool b = p.bf16[i];
-        V x = lds_vec<A>(stage + p.smem_off[i] + (size_t)vi * (b ? 8 : 16), b);
-        const uint8_t op = p.op[i];
-        st.push((op & RCV_OP_CANON) ? vcanon(x) : x);
-        const int merges = op & RCV_OP_MERGES_MASK;
-        for (int m = 0; m < merges; ++m) st.merge();
-      }
-      V r = st.s[0];
+        return lds_vec<A>(stage + p.smem_off[i] + (size_t)vi * (b ? 8 : 16), b);
+      };
+      V r = Prog::template eval<V>(p, ld);
       if (p.divisor != 0.0) r = vdiv(r, p.divisor);
       const unsigned long long off = (v0 + vi) * 16ull;
       for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + off, r);
@@ -569,7 +593,19 @@ struct FoldReq {
   char *out[RCV_MAX_OUT];
   int acc_dt = RCV_F32;
   double divisor = 0.0;
+  int tree_L = -1;  // >= 0: canonical tree tables below are valid
+  int8_t node_in[2 * RCV_MAX_IN - 1];
+  uint8_t present[2 * RCV_MAX_IN - 1];
 };
+
+enum { PK_STACK = 0, PK_LEFT = 1, PK_TREE = 2 };
+
+bool is_left_fold(const FoldReq &r) {
+  if (r.n_in < 1 || (r.op[0] & RCV_OP_MERGES_MASK)) return false;
+  for (int i = 1; i < r.n_in; ++i)
+    if (r.op[i] != 1) return false;
+  return true;
+}
 
 // simulate the program on the host: validates it and returns the max depth
 int program_depth(const uint8_t *ops, int n, int *max_depth) {
@@ -632,29 +668,23 @@ void fill_vec_params(FoldParams &p, const FoldReq &r, unsigned long long e0,
   for (int j = 0; j < r.n_out; ++j) p.out[j] = r.out[j] + e0 * sizeof(A);
   p.nvec = nvec;
   p.divisor = r.divisor;
+  if (r.tree_L >= 0) {
+    const int nodes = (2 << r.tree_L) - 1;
+    memcpy(p.node_in, r.node_in, nodes);
+    memcpy(p.present, r.present, nodes);
+  }
 }
 
-template <typename A, int MAXD>
-int launch_direct_t(const FoldReq &r, unsigned long long e0, unsigned long long nvec,
+template <typename A, typename Prog>
+int launch_direct_p(const FoldReq &r, unsigned long long e0, unsigned long long nvec,
                     cudaStream_t st, int sms) {
   FoldParams p;
   fill_vec_params<A>(p, r, e0, nvec);
-  constexpr int U = MAXD <= 2 ? 4 : (MAXD <= 4 ? 2 : 1);
-  const unsigned long long per_block = 256ull * U;
-  const unsigned long long want = (nvec + per_block - 1) / per_block;
+  const unsigned long long want = (nvec + 255) / 256;
   const unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)sms * 8));
-  fold_direct_kernel<A, MAXD, U><<<(unsigned)blocks, 256, 0, st>>>(p);
+  fold_direct_kernel<A, Prog><<<(unsigned)blocks, 256, 0, st>>>(p);
   CK(cudaGetLastError());
   return RCV_OK;
-}
-
-template <typename A>
-int launch_direct(const FoldReq &r, int maxd, unsigned long long e0, unsigned long long nvec,
-                  cudaStream_t st, int sms) {
-  if (maxd <= 2) return launch_direct_t<A, 2>(r, e0, nvec, st, sms);
-  if (maxd <= 4) return launch_direct_t<A, 4>(r, e0, nvec, st, sms);
-  if (maxd <= 8) return launch_direct_t<A, 8>(r, e0, nvec, st, sms);
-  return set_err(RCV_ERANGE, "fold program stack depth %d exceeds 8", maxd);
 }
 
 // TMA geometry: vectors-per-thread, stages, CTAs per SM
@@ -686,8 +716,8 @@ bool tma_geom(const FoldReq &r, TmaGeom *g) {
   return true;
 }
 
-template <typename A, int MAXD>
-int launch_tma_t(const FoldReq &r, const TmaGeom &g, unsigned long long e0,
+template <typename A, typename Prog>
+int launch_tma_p(const FoldReq &r, const TmaGeom &g, unsigned long long e0,
                  unsigned long long nvec, cudaStream_t st, int sms) {
   FoldParams p;
   fill_vec_params<A>(p, r, e0, nvec);
@@ -699,7 +729,7 @@ int launch_tma_t(const FoldReq &r, const TmaGeom &g, unsigned long long e0,
   p.stage_bytes = g.stage_bytes;
   p.stages = g.stages;
   p.vpt = g.vpt;
-  auto kern = fold_tma_kernel<A, MAXD>;
+  auto kern = fold_tma_kernel<A, Prog>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
   const unsigned long long tv = (unsigned long long)TMA_CONSUMERS * g.vpt;
   const unsigned long long ntiles = (nvec + tv - 1) / tv;
@@ -710,12 +740,28 @@ int launch_tma_t(const FoldReq &r, const TmaGeom &g, unsigned long long e0,
   return RCV_OK;
 }
 
+// Launch `variant` (TMA / DIRECT) of the best program policy for r.
 template <typename A>
-int launch_tma(const FoldReq &r, const TmaGeom &g, int maxd, unsigned long long e0,
-               unsigned long long nvec, cudaStream_t st, int sms) {
-  if (maxd <= 2) return launch_tma_t<A, 2>(r, g, e0, nvec, st, sms);
-  if (maxd <= 4) return launch_tma_t<A, 4>(r, g, e0, nvec, st, sms);
-  if (maxd <= 8) return launch_tma_t<A, 8>(r, g, e0, nvec, st, sms);
+int launch_vec(const FoldReq &r, bool tma, const TmaGeom &g, int maxd,
+               unsigned long long e0, unsigned long long nvec, cudaStream_t st, int sms) {
+#define RCV_LAUNCH(PROG) \
+  return tma ? launch_tma_p<A, PROG>(r, g, e0, nvec, st, sms) : launch_direct_p<A, PROG>(r, e0, nvec, st, sms)
+  if (r.tree_L >= 0 && r.tree_L <= 6) {
+    switch (r.tree_L) {
+      case 0: RCV_LAUNCH(ProgTree<0>);
+      case 1: RCV_LAUNCH(ProgTree<1>);
+      case 2: RCV_LAUNCH(ProgTree<2>);
+      case 3: RCV_LAUNCH(ProgTree<3>);
+      case 4: RCV_LAUNCH(ProgTree<4>);
+      case 5: RCV_LAUNCH(ProgTree<5>);
+      default: RCV_LAUNCH(ProgTree<6>);
+    }
+  }
+  if (is_left_fold(r)) RCV_LAUNCH(ProgLeft);
+  if (maxd <= 2) RCV_LAUNCH(ProgStack<2>);
+  if (maxd <= 4) RCV_LAUNCH(ProgStack<4>);
+  if (maxd <= 8) RCV_LAUNCH(ProgStack<8>);
+#undef RCV_LAUNCH
   return set_err(RCV_ERANGE, "fold program stack depth %d exceeds 8", maxd);
 }
 
@@ -763,10 +809,8 @@ int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int s
         return set_err(RCV_EINVAL, "TMA variant: %d inputs do not fit a 2-stage ring", r.n_in);
       use_tma = false;
     }
-    if (use_tma)
-      rc = f64 ? launch_tma<double>(r, g, maxd, h, nvec, st, sms) : launch_tma<float>(r, g, maxd, h, nvec, st, sms);
-    else
-      rc = f64 ? launch_direct<double>(r, maxd, h, nvec, st, sms) : launch_direct<float>(r, maxd, h, nvec, st, sms);
+    rc = f64 ? launch_vec<double>(r, use_tma, g, maxd, h, nvec, st, sms)
+             : launch_vec<float>(r, use_tma, g, maxd, h, nvec, st, sms);
     if (rc) return rc;
   }
   if (body_end < numel) {
@@ -1037,6 +1081,23 @@ int rcv_tree_commit(const rcv_block *blocks, int n_blocks, uint32_t n_leaves,
   }
   r.n_out = n_out;
   for (int j = 0; j < n_out; ++j) r.out[j] = (char *)out[j];
+  uint32_t L = 0;
+  while ((1ull << L) < n_leaves) ++L;
+  if (L <= 6) {  // compile-time tree kernels cover up to 64 leaves
+    const int nodes = (2 << L) - 1;
+    memset(r.node_in, -1, sizeof r.node_in);
+    memset(r.present, 0, sizeof r.present);
+    for (int i = 0; i < n_blocks; ++i) {
+      const int id = (1 << (L - lev[i])) - 1 + (int)(lo[i] >> lev[i]);
+      r.node_in[id] = (int8_t)i;
+      r.present[id] = 1;
+    }
+    // a node is present when it or any descendant is fed; ids of children of
+    // node id are 2id+1, 2id+2, so sweep from the leaves upward
+    for (int id = nodes - 1; id > 0; --id)
+      if (r.present[id]) r.present[(id - 1) / 2] = 1;
+    r.tree_L = (int)L;
+  }
   return run_fold(r, numel, variant, (cudaStream_t)stream, current_device_sms());
 }
 
