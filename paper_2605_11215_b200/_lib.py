@@ -303,4 +303,4 @@ def toy_grad(linear: bool, params: torch.Tensor, lanes: torch.Tensor,
                                wstar.data_ptr() if wstar is not None else None,
                                dim, grad.data_ptr() if grad is not None else None,
                                scal.data_ptr(),
-                               stream_of(grad)))
+                               stream_of(scal)))

@@ -261,6 +261,26 @@ template <int L> struct ProgTree {
   }
 };
 
+// Full canonical tree: input i is leaf i of a perfect tree of height L (the
+// failure-free cover, and every canonical recompute cover). Branch-free and
+// straight-line: 2^L loads, 2^L - 1 adds, all indices compile-time.
+template <int L> struct ProgFull {
+  template <int LEVEL, int IDX, typename V, typename Ld>
+  __device__ __forceinline__ static V node(const Ld &ld) {
+    if constexpr (LEVEL == 0) {
+      return ld(IDX);
+    } else {
+      const V a = node<LEVEL - 1, 2 * IDX, V>(ld);
+      const V b = node<LEVEL - 1, 2 * IDX + 1, V>(ld);
+      return vadd(a, b);
+    }
+  }
+  template <typename V, typename Ld>
+  __device__ __forceinline__ static V eval(const FoldParams &, const Ld &ld) {
+    return node<L, 0, V>(ld);
+  }
+};
+
 // ---------------------------------------------------------------------------
 // DIRECT variant: 128-bit LDG straight from (local or peer) global memory
 
@@ -594,6 +614,7 @@ struct FoldReq {
   int acc_dt = RCV_F32;
   double divisor = 0.0;
   int tree_L = -1;  // >= 0: canonical tree tables below are valid
+  int full_L = -1;  // >= 0: inputs are the 2^full_L leaves of a perfect tree
   int8_t node_in[2 * RCV_MAX_IN - 1];
   uint8_t present[2 * RCV_MAX_IN - 1];
 };
@@ -746,6 +767,17 @@ int launch_vec(const FoldReq &r, bool tma, const TmaGeom &g, int maxd,
                unsigned long long e0, unsigned long long nvec, cudaStream_t st, int sms) {
 #define RCV_LAUNCH(PROG) \
   return tma ? launch_tma_p<A, PROG>(r, g, e0, nvec, st, sms) : launch_direct_p<A, PROG>(r, e0, nvec, st, sms)
+  if (r.full_L >= 0 && r.full_L <= 6) {
+    switch (r.full_L) {
+      case 0: RCV_LAUNCH(ProgFull<0>);
+      case 1: RCV_LAUNCH(ProgFull<1>);
+      case 2: RCV_LAUNCH(ProgFull<2>);
+      case 3: RCV_LAUNCH(ProgFull<3>);
+      case 4: RCV_LAUNCH(ProgFull<4>);
+      case 5: RCV_LAUNCH(ProgFull<5>);
+      default: RCV_LAUNCH(ProgFull<6>);
+    }
+  }
   if (r.tree_L >= 0 && r.tree_L <= 6) {
     switch (r.tree_L) {
       case 0: RCV_LAUNCH(ProgTree<0>);
@@ -1097,6 +1129,16 @@ int rcv_tree_commit(const rcv_block *blocks, int n_blocks, uint32_t n_leaves,
     for (int id = nodes - 1; id > 0; --id)
       if (r.present[id]) r.present[(id - 1) / 2] = 1;
     r.tree_L = (int)L;
+    // all blocks at one level, all present, in order: a perfect tree of
+    // height L - level over the inputs themselves
+    bool full = n_blocks > 0 && (n_blocks & (n_blocks - 1)) == 0;
+    for (int i = 0; i < n_blocks && full; ++i)
+      full = lev[i] == lev[0] && lo[i] == ((uint32_t)i << lev[0]);
+    if (full && ((uint32_t)n_blocks << lev[0]) == (1u << L)) {
+      int fl = 0;
+      while ((1 << fl) < n_blocks) ++fl;
+      r.full_L = fl;
+    }
   }
   return run_fold(r, numel, variant, (cudaStream_t)stream, current_device_sms());
 }
