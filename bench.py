@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--numel", type=int, default=D_GPT2)
     ap.add_argument("--no-fail", action="store_true")
     ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--combine-variant", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sample", type=int, default=1 << 23)
     ap.add_argument("--skip-cpu", action="store_true")
@@ -265,13 +266,20 @@ def run_ours(args):
     numel = args.numel
 
     # synthetic per-microbatch gradients (the backward outputs), in HBM
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    # the same generator sequence on every rank: microbatch m's gradient has
+    # the same bits wherever it is (re)computed (canonical addressing)
+    gen = torch.Generator(device=dev).manual_seed(1234)
     leaves = [torch.randn(numel, generator=gen, device=dev, dtype=torch.float32)
               for _ in range(M)]
     total_steps = args.warmup + args.steps
     fail_step = -1 if args.no_fail else args.warmup + args.steps // 2
-    eng = GradientCommit(numel, W, G, K, placement={r: dev for r in range(W)},
-                         variant=args.variant)
+    if world > 1:
+        from paper_2605_11215_b200.dist import DistributedGradientCommit
+        eng = DistributedGradientCommit(numel, W, G, K, variant=args.variant,
+                                        combine_variant=args.combine_variant)
+    else:
+        eng = GradientCommit(numel, W, G, K, placement={r: dev for r in range(W)},
+                             variant=args.variant)
     kill = StepKill(fail_step)
 
     def leaf(m, rid):
@@ -314,11 +322,26 @@ def run_ours(args):
     tokens = committed * TOKENS_PER_MB
     value = tokens / (elapsed_ms / 1e3)
 
-    # roofline of the fused commit kernel over the timed region
-    durs = [a.elapsed_time(z) for a, z, _ in eng.timing]
-    nbytes = [b for _, _, b in eng.timing]
-    achieved = sum(nbytes) / (sum(durs) / 1e3) / 1e9 if durs else None
+    # roofline per kernel kind over the timed region (CUDA events on the
+    # launching stream around every launch)
+    kinds = {}
+    for a, z, nb, kind, (nin, nout) in eng.timing:
+        k = kinds.setdefault(kind, {"launches": 0, "ms": 0.0, "bytes": 0, "nvl_in": 0, "nvl_out": 0})
+        k["launches"] += 1
+        k["ms"] += a.elapsed_time(z)
+        k["bytes"] += nb
+        k["nvl_in"] += nin
+        k["nvl_out"] += nout
     peak, peak_kind = peaks()
+    per_kind = {}
+    for kind, k in kinds.items():
+        sec = k["ms"] / 1e3
+        per_kind[kind] = {
+            "launches": k["launches"], "mean_launch_us": 1e3 * k["ms"] / k["launches"],
+            "hbm_gbs": k["bytes"] / sec / 1e9 if sec else None,
+            "nvlink_in_gbs": k["nvl_in"] / sec / 1e9 if sec else None,
+            "nvlink_out_gbs": k["nvl_out"] / sec / 1e9 if sec else None}
+    dom = max(kinds, key=lambda kk: kinds[kk]["ms"]) if kinds else None
     fail_idx = [i for i, o in enumerate(outcomes) if o.events]
     normal = [ms for i, ms in enumerate(step_ms) if i not in fail_idx]
     recovery_ms = (step_ms[fail_idx[0]] - statistics.median(normal)) if fail_idx and normal else None
@@ -326,14 +349,16 @@ def run_ours(args):
 
     # correctness spot check inside the bench: every live replica holds the
     # same bytes (one kernel wrote them all)
-    ref = eng.grads[eng.comm.members[0]]
-    agree = all(torch.equal(eng.grads[r], ref) for r in eng.comm.members[1:])
+    mine = [r for r in eng.comm.members if r in eng.grads]
+    agree = all(torch.equal(eng.grads[r], eng.grads[mine[0]]) for r in mine[1:])
 
     # e2e through the public API with host buffers: pinned host gradients
     # copied in every step, committed gradient copied out every step
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and world == 1:
         e2e = e2e_leg(args, dev, leaves, numel)
+    if world > 1:
+        eng.check_peers()
 
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
@@ -346,19 +371,16 @@ def run_ours(args):
                    "numel": numel, "replicas": W, "microbatches": M, "buckets": K,
                    "tokens_per_microbatch": TOKENS_PER_MB,
                    "fail_step": fail_step, "placement": "8 replicas on 1 GPU" if world == 1
-                   else "replicas per rank", "l2": "inputs 15.9 GB >> 126 MB L2",
+                   else "%d replicas per rank, NVLink P2P" % (W // world), "l2": "inputs 15.9 GB >> 126 MB L2",
                    "parallelism": "dp8-sim"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None, "traffic": None,
-                     "peak_kind": peak_kind, "kernel": "fold_tma_kernel (rcv_tree_commit)",
-                     "launches_timed": len(durs),
-                     "mean_launch_us": 1e3 * sum(durs) / len(durs) if durs else None},
-        "allreduce_gbs": achieved,
+        "roofline": roofline(dom, per_kind, peak, peak_kind),
+        "kernels": per_kind,
+        "allreduce_gbs": per_kind.get("combine", per_kind.get("fused", {})).get("hbm_gbs"),
         "recovery_ms": recovery_ms,
         "step_ms": {"median": statistics.median(step_ms), "max": max(step_ms),
                     "failure_step": step_ms[fail_idx[0]] if fail_idx else None},
         "replica_agreement": agree,
-        "gpu_launches": launches,
+        "gpu_launches": launches + getattr(eng, "barriers", 0),
         "clocks": clk.summary(),
         "e2e": e2e,
     }
@@ -371,6 +393,27 @@ def run_ours(args):
         print(json.dumps(line))
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+NVLINK_PEAK = 770.0  # GB/s per direction, measured peer copy (B200_PROFILING.md)
+TRAFFIC = {"fused": 977.8e6}  # dram read+write bytes per launch, ncu --set full (profiles/r1)
+
+
+def roofline(dom, per_kind, peak, peak_kind):
+    if dom is None:
+        return None
+    k = per_kind[dom]
+    if dom == "combine" and (k["nvlink_in_gbs"] or 0) > 0:
+        ach = max(k["nvlink_in_gbs"], k["nvlink_out_gbs"])
+        return {"bound": "nvlink", "achieved": ach, "peak": NVLINK_PEAK, "unit": "GB/s",
+                "frac": ach / NVLINK_PEAK, "traffic": None, "peak_kind": "measured peer copy",
+                "kernel": "fold_tma_kernel combine (rcv_tree_commit over peer pointers)",
+                "hbm_gbs": k["hbm_gbs"]}
+    return {"bound": "hbm", "achieved": k["hbm_gbs"], "peak": peak, "unit": "GB/s",
+            "frac": k["hbm_gbs"] / peak if k["hbm_gbs"] else None,
+            "traffic": TRAFFIC.get(dom), "peak_kind": peak_kind,
+            "kernel": "fold_tma_kernel<float, ProgFull<5>> (rcv_tree_commit, %s)" % dom,
+            "mean_launch_us": k["mean_launch_us"], "launches_timed": k["launches"]}
 
 
 def e2e_leg(args, dev, leaves, numel):

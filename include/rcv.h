@@ -175,6 +175,32 @@ int rcv_toy_grad(int kind_linear, const double *params, const double *lanes,
                  const double *wstar, size_t dim, double *grad, double *scal,
                  void *stream);
 
+/* ---- multi-process (one process per GPU) -------------------------------
+ * The reference has no processes (comm.py:1-9: collectives are atomic rounds
+ * of one interpreter); these entry points are what a ProcessGroupULFM-style
+ * backend binds instead: buffers shared between the rank
+ * processes of one node over NVLink, and a stream-ordered flag barrier whose
+ * spin is bounded, so a peer that stopped responding is reported as a status
+ * bit instead of hanging the GPU (the crash-stop detection of comm.py:129). */
+
+/* Export the allocation containing `ptr` (cudaIpcGetMemHandle); handle_out
+ * receives 64 bytes, *offset_out the offset of ptr inside the allocation. */
+int rcv_ipc_export(const void *ptr, void *handle_out, size_t *offset_out);
+
+/* Map a peer's exported allocation (cached per handle) and return the device
+ * pointer to base + offset in this process. */
+int rcv_ipc_import(const void *handle, size_t offset, void **ptr_out);
+
+/* Cross-GPU barrier among the ranks in live_mask: rank `me` stores `value`
+ * into slot `me` of every live peer's flag array (peer_flags[r], mapped
+ * pointers), then waits until its own local_flags[r] >= value for every live
+ * peer r, each wait bounded by timeout_ns of %globaltimer.  A peer that times
+ * out sets bit r in *status (device uint32) instead of blocking forever.
+ * Launched on `stream`, ordered after the caller's prior work. */
+int rcv_barrier(uint64_t *local_flags, void *const *peer_flags, int n, int me,
+                uint64_t live_mask, uint64_t value, uint64_t timeout_ns,
+                uint32_t *status, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,6 +29,7 @@ EXPORTS = (
     "rcv_masked_allreduce_multidev", "rcv_accumulate", "rcv_tree_commit",
     "rcv_tree_program", "rcv_copy", "rcv_zero", "rcv_compare",
     "rcv_sgd_commit", "rcv_unit_lanes", "rcv_toy_grad",
+    "rcv_ipc_export", "rcv_ipc_import", "rcv_barrier",
 )
 
 
@@ -83,6 +84,9 @@ def load() -> ctypes.CDLL:
         "rcv_unit_lanes": (i32, [vp, u64, sz, ctypes.c_double,
                                  ctypes.c_double, i32, vp]),
         "rcv_toy_grad": (i32, [i32, vp, vp, vp, sz, vp, vp, vp]),
+        "rcv_ipc_export": (i32, [vp, vp, ctypes.POINTER(sz)]),
+        "rcv_ipc_import": (i32, [vp, sz, ctypes.POINTER(vp)]),
+        "rcv_barrier": (i32, [vp, pvp, i32, i32, u64, u64, u64, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -304,3 +308,48 @@ def toy_grad(linear: bool, params: torch.Tensor, lanes: torch.Tensor,
                                dim, grad.data_ptr() if grad is not None else None,
                                scal.data_ptr(),
                                stream_of(scal)))
+
+
+# ---- multi-process helpers -------------------------------------------------
+
+def ipc_export(t: torch.Tensor):
+    """(64-byte handle, offset) of the allocation holding t."""
+    require_cuda(t.view(-1) if t.dim() != 1 else t, "shared buffer")
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_size_t(0)
+    _check(load().rcv_ipc_export(t.data_ptr(), h, ctypes.byref(off)))
+    return h.raw, off.value
+
+
+def ipc_import(handle: bytes, offset: int) -> int:
+    ptr = ctypes.c_void_p(0)
+    buf = ctypes.create_string_buffer(handle, 64)
+    _check(load().rcv_ipc_import(buf, offset, ctypes.byref(ptr)))
+    return ptr.value
+
+
+def barrier(local_flags: torch.Tensor, peer_flag_ptrs: Sequence[int], me: int,
+            live_mask: int, value: int, timeout_ns: int,
+            status: torch.Tensor) -> None:
+    n = len(peer_flag_ptrs)
+    arr = (ctypes.c_void_p * n)(*peer_flag_ptrs)
+    _check(load().rcv_barrier(local_flags.data_ptr(), arr, n, me, live_mask,
+                              value, timeout_ns, status.data_ptr(),
+                              stream_of(local_flags)))
+
+
+def tree_commit_raw(blocks: Sequence[tuple], n_leaves: int,
+                    out_ptrs: Sequence[int], numel: int, acc_dtype: int,
+                    divisor: float, stream: int,
+                    variant: int = VARIANT_AUTO) -> None:
+    """tree_commit over raw device pointers (peer-mapped allowed):
+    blocks = [(ptr, lo, level, dtype)], ascending lo."""
+    if not out_ptrs or numel == 0:
+        return
+    arr = (_Block * max(1, len(blocks)))()
+    for i, (ptr, lo, level, dt) in enumerate(blocks):
+        arr[i] = _Block(ptr, lo, level, dt)
+    outs = (ctypes.c_void_p * len(out_ptrs))(*out_ptrs)
+    _check(load().rcv_tree_commit(arr, len(blocks), n_leaves, len(out_ptrs),
+                                  outs, acc_dtype, numel, float(divisor),
+                                  variant, stream))

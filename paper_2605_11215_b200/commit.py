@@ -143,11 +143,19 @@ class GradientCommit:
         self.grads = {r: torch.empty(numel, dtype=dtype, device=self.placement[r])
                       for r in members}
         self._scratch: Dict[torch.device, List[torch.Tensor]] = {}
-        # optional launch timing: list of (start_event, end_event, algo_bytes)
+        # optional launch timing: list of (start_event, end_event, algo_bytes, kind)
         self.timing: Optional[list] = None
         _lib.enable_peer_access(sorted({d.index for d in self.placement.values()}))
 
     # ---- data plane ----
+
+    def _holds(self, rid: int) -> bool:
+        """Whether this process holds replica rid's buffers (all of them in
+        single-process mode; the distributed engine overrides)."""
+        return True
+
+    def _end_of_step(self) -> None:
+        """Hook run after the last bucket of a step is committed."""
 
     def _scratch_buf(self, dev: torch.device, i: int, n: int) -> torch.Tensor:
         pool = self._scratch.setdefault(dev, [])
@@ -215,7 +223,7 @@ class GradientCommit:
         a.record()
         launch()
         z.record()
-        self.timing.append((a, z, nbytes))
+        self.timing.append((a, z, nbytes, "fused", (0, 0)))
 
     def _on_device(self, outs, dev, launch, extra=()):
         """Run ``launch`` on dev's current stream, ordered after the other
@@ -333,7 +341,7 @@ class GradientCommit:
                 if comm.roles[rid] in SPARE_ROLES and not comm.boundary_latch:
                     continue      # virtual zeroing: spare work never enters
                 for i in admitted.get(rid, ()):
-                    lv[i] = (rid, leaf(i, rid))
+                    lv[i] = (rid, leaf(i, rid) if self._holds(rid) else None)
             return lv
 
         def reduce(k: int) -> WorkResult:
@@ -441,6 +449,7 @@ class GradientCommit:
             if m >= p_major:
                 break
 
+        self._end_of_step()
         # ---- commit ----
         members = list(comm.members)
         reg, bdy = comm.census_contrib()

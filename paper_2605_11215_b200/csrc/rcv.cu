@@ -25,6 +25,7 @@
 // Fold order is exact: every add is __fadd_rn/__dadd_rn in program order,
 // the final scale is __fdiv_rn/__ddiv_rn (IEEE true division, like numpy).
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdarg.h>
@@ -576,6 +577,51 @@ __global__ void toy_grad_kernel(int linear, const double *lanes,
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
        i < dim; i += (unsigned long long)gridDim.x * blockDim.x)
     grad[i] = linear ? __dmul_rn(r, lanes[i]) : lanes[i];
+}
+
+// ---------------------------------------------------------------------------
+// cross-GPU flag barrier (multi-process mode)
+
+struct BarrierParams {
+  unsigned long long *peer[RCV_MAX_OUT];
+  unsigned long long *local;
+  unsigned int *status;
+  unsigned long long live;
+  unsigned long long value;
+  unsigned long long timeout_ns;
+  int n;
+  int me;
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
+  const int t = threadIdx.x;
+  const bool peer = t < p.n && t != p.me && ((p.live >> t) & 1ull);
+  // everything this GPU wrote before this kernel (partials, remote stores)
+  // is made visible system-wide before the flag store releases it
+  __threadfence_system();
+  if (peer)
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.peer[t] + p.me), "l"(p.value)
+                 : "memory");
+  if (peer) {
+    const unsigned long long t0 = globaltimer();
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.local + t) : "memory");
+      if (v >= p.value) break;
+      if (globaltimer() - t0 > p.timeout_ns) {
+        atomicOr(p.status, 1u << (t & 31));
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -1141,6 +1187,71 @@ int rcv_tree_commit(const rcv_block *blocks, int n_blocks, uint32_t n_leaves,
     }
   }
   return run_fold(r, numel, variant, (cudaStream_t)stream, current_device_sms());
+}
+
+int rcv_ipc_export(const void *ptr, void *handle_out, size_t *offset_out) {
+  void *base = nullptr;
+  size_t size = 0;
+  CUdeviceptr b = 0;
+  // the allocation holding ptr (torch's caching allocator sub-allocates);
+  // the driver symbol is resolved at run time so the library loads on hosts
+  // without libcuda (the CPU build box)
+  typedef CUresult (*range_fn)(CUdeviceptr *, size_t *, CUdeviceptr);
+  static range_fn get_range = nullptr;
+  if (!get_range) {
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn)
+      return set_err(RCV_ECUDA, "cuMemGetAddressRange unavailable");
+    get_range = (range_fn)fn;
+  }
+  if (get_range(&b, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS)
+    return set_err(RCV_EINVAL, "ipc export: %p is not a device allocation", ptr);
+  base = (void *)b;
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, base));
+  memcpy(handle_out, &h, sizeof h);
+  *offset_out = (size_t)((const char *)ptr - (const char *)base);
+  return RCV_OK;
+}
+
+int rcv_ipc_import(const void *handle, size_t offset, void **ptr_out) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::string, void *>> opened;
+  std::lock_guard<std::mutex> lk(mu);
+  const std::string key((const char *)handle, sizeof(cudaIpcMemHandle_t));
+  for (auto &e : opened)
+    if (e.first == key) {
+      *ptr_out = (char *)e.second + offset;
+      return RCV_OK;
+    }
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  void *base = nullptr;
+  CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  opened.emplace_back(key, base);
+  *ptr_out = (char *)base + offset;
+  return RCV_OK;
+}
+
+int rcv_barrier(uint64_t *local_flags, void *const *peer_flags, int n, int me,
+                uint64_t live_mask, uint64_t value, uint64_t timeout_ns,
+                uint32_t *status, void *stream) {
+  if (n < 1 || n > 32 || me < 0 || me >= n) return set_err(RCV_ERANGE, "barrier: n %d me %d", n, me);
+  BarrierParams p;
+  memset(&p, 0, sizeof p);
+  for (int r = 0; r < n; ++r) p.peer[r] = (unsigned long long *)peer_flags[r];
+  p.local = (unsigned long long *)local_flags;
+  p.status = status;
+  p.live = live_mask;
+  p.value = value;
+  p.timeout_ns = timeout_ns;
+  p.n = n;
+  p.me = me;
+  barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
+  CK(cudaGetLastError());
+  return RCV_OK;
 }
 
 int rcv_copy(void *dst, const void *src, size_t bytes, void *stream) {

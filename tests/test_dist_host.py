@@ -1,0 +1,82 @@
+"""Host logic of the multi-process commit on CPU: a world-2 gloo group runs
+the replicated control plane and the per-bucket plan on both ranks and
+checks they agree (same decisions, same cover, disjoint owner slices)."""
+
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2605_11215_b200.dist import owner_slice, plan_bucket
+
+
+def test_owner_slices_partition():
+    for n in (0, 1, 63, 64, 65, 1000, 6221990):
+        for nr in (1, 2, 3, 4, 7, 8):
+            spans = [owner_slice(n, q, nr) for q in range(nr)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            for (a, z), (a2, _) in zip(spans, spans[1:]):
+                assert z == a2 and a % 64 == 0
+
+
+def test_plan_failure_layout():
+    # 8 replicas x 4 microbatches on 2 ranks, replica 3 dead, its 4 indices
+    # recomputed by survivors 0, 1, 2 (rank 0) and 4 (rank 1)
+    rank_of = {r: r // 4 for r in range(8)}
+    holder = {m: m // 4 for m in range(32)}
+    for m, r in zip(range(12, 16), (0, 1, 2, 4)):
+        holder[m] = r
+    owner = {m: rank_of[r] for m, r in holder.items()}
+    cover, slot_of = plan_bucket(owner, 32, [0, 1], pool_slots=8)
+    assert cover == [(0, 3), (8, 2), (12, 1), (14, 0), (15, 0), (16, 4)]
+    assert [slot_of[c][0] for c in cover] == [0, 0, 0, 0, 1, 1]
+    with pytest.raises(RuntimeError):
+        plan_bucket(owner, 32, [0], pool_slots=8)     # rank 1 is not live
+    with pytest.raises(RuntimeError):
+        plan_bucket(owner, 32, [0, 1], pool_slots=2)  # rank 0 needs 4 slots
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_11215_b200.comm import Communicator
+    from paper_2605_11215_b200.policy import assign_roles, initial_state
+    # replicated control plane: both ranks run the same failure schedule
+    st = initial_state(8, 4)
+    comm = Communicator(range(8), assign_roles(st, list(range(8))))
+    for r in comm.members:
+        comm.contrib_regular[r] = 4
+    comm.mark_dead(3)
+    rec = comm.ulfm_consensus().record
+    rank_of = {r: r // (8 // world) for r in range(8)}
+    owner = {m: rank_of[min(m // 4, 7)] for m in range(32) if m // 4 in comm.members}
+    live = sorted({rank_of[r] for r in comm.members})
+    cover, slot_of = plan_bucket(owner, 32, live, 8)
+    mine = owner_slice(6221990, live.index(rank), len(live))
+    got = [None] * world
+    dist.all_gather_object(got, (rec.contrib, rec.at_boundary, cover,
+                                 sorted(slot_of.items()), mine))
+    dist.destroy_process_group()
+    q.put((rank, got))
+
+
+def test_replicated_plan_agrees_world2():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a, b = res[0][0], res[0][1]
+    assert a[:4] == b[:4]                 # same decision and plan on both ranks
+    assert a[0] == 28 and a[1] is True    # census of 7 survivors x 4
+    assert a[4][1] == b[4][0] and a[4][0] == 0 and b[4][1] == 6221990

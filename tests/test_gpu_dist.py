@@ -1,0 +1,78 @@
+"""Multi-process commit on >= 2 GPUs (one process per GPU, NCCL group for
+the handle exchange, NVLink P2P for the data): the committed gradient on
+every rank equals the CPU oracle's canonical tree bit for bit, with and
+without a replica death, for both combine variants."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+
+def _worker(rank, world, port, combine_variant, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        from paper_2605_11215_b200.dist import DistributedGradientCommit
+        from oracle import fold
+        numel = 5 * 64 * 37 + 19
+        host = [np.random.default_rng(100 + m).standard_normal(numel).astype(np.float32)
+                for m in range(32)]
+        dev = [torch.from_numpy(h).cuda() for h in host]
+        want = fold.canonical_tree(dict(enumerate(host)), 32) / np.float32(32)
+        eng = DistributedGradientCommit(numel, 8, 4, 5, combine_variant=combine_variant)
+
+        class Kill:
+            def __init__(self, plan):
+                self.plan = list(plan)
+
+            def fire(self, phase, bucket=None):
+                hit = [e for e in self.plan if e[0] == phase and (phase != "during_sync" or e[1] == bucket)]
+                self.plan = [e for e in self.plan if e not in hit]
+                return [r for e in hit for r in e[2]]
+
+        results = []
+        for t, plan in enumerate([[], [("during_sync", 2, [3])], [], [("before_sync", None, [6])]]):
+            out = eng.step(t, lambda m, rid: dev[m], Kill(plan))
+            torch.cuda.synchronize()
+            ok = all(eng.grads[r].cpu().numpy().tobytes() == want.tobytes()
+                     for r in eng.comm.members if eng._holds(r))
+            results.append((ok, out.contrib_total, sorted(out.contributions.items())))
+        eng.check_peers()
+        q.put((rank, results))
+    except Exception as exc:  # surface the error to the parent
+        q.put((rank, repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("combine_variant", [0, 2])
+def test_distributed_commit_bitwise(combine_variant):
+    world = min(torch.cuda.device_count(), 4)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = torch.multiprocessing.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, combine_variant, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert not isinstance(res[r], str), res[r]
+        for ok, total, contrib in res[r]:
+            assert ok and total == 32
+    assert res[0] == res[world - 1]
+    # after replica 3 died: advanced 7-replica layout, G = 5 and a minor at 2
+    assert res[0][2][2] == [(0, 5), (1, 5), (2, 5), (4, 5), (5, 5), (6, 5), (7, 2)]
