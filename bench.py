@@ -375,7 +375,9 @@ def run_ours(args):
                    "parallelism": "dp8-sim"},
         "roofline": roofline(dom, per_kind, peak, peak_kind),
         "kernels": per_kind,
-        "allreduce_gbs": per_kind.get("combine", per_kind.get("fused", {})).get("hbm_gbs"),
+        # masked-allreduce algorithmic bandwidth: gradient bytes committed
+        # (reduced over the live replicas and scaled) per second of step time
+        "allreduce_algbw_gbs": numel * 4 / (elapsed_ms / args.steps / 1e3) / 1e9,
         "recovery_ms": recovery_ms,
         "step_ms": {"median": statistics.median(step_ms), "max": max(step_ms),
                     "failure_step": step_ms[fail_idx[0]] if fail_idx else None},

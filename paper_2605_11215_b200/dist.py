@@ -15,8 +15,11 @@ crosses GPUs:
 3. *combine* — each live rank owns one 64-element-aligned slice of the
    bucket: it reads every cover node's partial slice (peers' over NVLink),
    evaluates the top of the canonical tree, divides by B and stores the
-   slice into every live replica's gradient buffer (peers' over NVLink) —
-   reduce-scatter and all-gather fused in one launch.
+   slice into the primary replica buffer of every live rank (peers' over
+   NVLink) — reduce-scatter and all-gather fused in one launch;
+4. *local broadcast* — after the next barrier each rank copies the bucket
+   from its primary replica into its other replicas (HBM), so NVLink carries
+   one copy per rank, not one per replica.
 
 Partial pools are double-buffered by call parity, so one barrier per bucket
 suffices (a rank passing barrier k+1 has finished combine k); one more
@@ -137,6 +140,7 @@ class DistributedGradientCommit(GradientCommit):
         self.flag_ptr = pb.share(self.flags)
         self._seq = 0
         self._calls = 0
+        self._pending = None  # (lo, hi) of the last combined bucket to broadcast locally
         self.barriers = 0  # barrier kernels launched (for launch accounting)
         torch.cuda.synchronize(self.device)
         dist.barrier(group=group)
@@ -149,9 +153,30 @@ class DistributedGradientCommit(GradientCommit):
     def _live_ranks(self) -> List[int]:
         return sorted({self.rank_of[r] for r in self.comm.members})
 
+    def _primary(self, rank: int) -> Optional[int]:
+        """Lowest live replica on `rank`: the one the combine stores into."""
+        return next((r for r in self.comm.members if self.rank_of[r] == rank), None)
+
+    def _flush_broadcast(self) -> None:
+        """Copy the last combined bucket from this rank's primary replica to
+        its other live replicas (HBM only).  Runs after a barrier, so every
+        peer's stores into the primary have landed."""
+        if self._pending is None:
+            return
+        lo, hi = self._pending
+        self._pending = None
+        mine = [r for r in self.comm.members if self._holds(r)]
+        if len(mine) < 2:
+            return
+        src = self.grads[mine[0]][lo:hi]
+        outs = [self.grads[r][lo:hi] for r in mine[1:]]
+        self._timed_launch("broadcast", (1 + len(outs)) * (hi - lo) * self._es,
+                           lambda: _lib.fold([src], [0], outs, variant=self.variant))
+
     def _barrier(self) -> None:
         ranks = self._live_ranks()
         if self.rank not in ranks or len(ranks) < 2:
+            self._flush_broadcast()
             return
         self._seq += 1
         self.barriers += 1
@@ -160,6 +185,7 @@ class DistributedGradientCommit(GradientCommit):
             mask |= 1 << r
         _lib.barrier(self.flags, self.flag_ptr, self.rank, mask, self._seq,
                      self.timeout_ns, self.status)
+        self._flush_broadcast()
 
     def _end_of_step(self) -> None:
         self._barrier()
@@ -220,14 +246,16 @@ class DistributedGradientCommit(GradientCommit):
             if z > a:
                 blocks = [(self._pool_at(rk, set_idx, j, a), blo, blev, self._code)
                           for (blo, blev), (rk, j) in sorted(slot_of.items())]
-                outs = [self.grad_ptr[r] + (lo + a) * self._es for r in members]
+                prim = [self._primary(rk) for rk in ranks]
+                outs = [self.grad_ptr[r] + (lo + a) * self._es for r in prim]
                 stream = torch.cuda.current_stream(self.device).cuda_stream
                 sl = (z - a) * self._es
                 remote_in = sum(1 for rk, _ in slot_of.values() if rk != self.rank)
-                remote_out = sum(1 for r in members if not self._holds(r))
+                remote_out = sum(1 for r in prim if not self._holds(r))
                 local = (len(blocks) - remote_in) + (len(outs) - remote_out)
                 self._timed_launch("combine", local * sl, lambda: _lib.tree_commit_raw(
                     blocks, b, outs, z - a, self._code, float(b), stream,
                     self.combine_variant), nvlink=(remote_in * sl, remote_out * sl))
                 launches += 1
+        self._pending = (lo, hi)
         return launches
