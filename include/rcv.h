@@ -129,6 +129,17 @@ int rcv_tree_commit(const rcv_block *blocks, int n_blocks, uint32_t n_leaves,
                     int n_out, void *const *out, int acc_dtype, size_t numel,
                     double divisor, int variant, void *stream);
 
+/* rcv_tree_commit on sub-ranges: every block pointer is advanced by
+ * in_offset elements (of its own dtype) and every output by out_offset
+ * elements, so a caller can prebuild the pointer arrays once per plan and
+ * commit bucket after bucket (or owner slice after owner slice) with two
+ * integers — the per-bucket host cost is one call. */
+int rcv_tree_commit_at(const rcv_block *blocks, int n_blocks,
+                       uint32_t n_leaves, int n_out, void *const *out,
+                       int acc_dtype, size_t in_offset, size_t out_offset,
+                       size_t numel, double divisor, int variant,
+                       void *stream);
+
 /* Host-side helper: the post-order fold program for rcv_tree_commit, exposed
  * so tests can check it without a GPU.  ops_out must hold n_blocks bytes;
  * blocks are taken in ascending `lo` order (the caller sorts). Returns the

@@ -29,7 +29,7 @@ EXPORTS = (
     "rcv_masked_allreduce_multidev", "rcv_accumulate", "rcv_tree_commit",
     "rcv_tree_program", "rcv_copy", "rcv_zero", "rcv_compare",
     "rcv_sgd_commit", "rcv_unit_lanes", "rcv_toy_grad",
-    "rcv_ipc_export", "rcv_ipc_import", "rcv_barrier",
+    "rcv_ipc_export", "rcv_ipc_import", "rcv_barrier", "rcv_tree_commit_at",
 )
 
 
@@ -87,6 +87,8 @@ def load() -> ctypes.CDLL:
         "rcv_ipc_export": (i32, [vp, vp, ctypes.POINTER(sz)]),
         "rcv_ipc_import": (i32, [vp, sz, ctypes.POINTER(vp)]),
         "rcv_barrier": (i32, [vp, pvp, i32, i32, u64, u64, u64, vp, vp]),
+        "rcv_tree_commit_at": (i32, [ctypes.POINTER(_Block), i32, u32, i32, pvp,
+                                     i32, sz, sz, sz, ctypes.c_double, i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -353,3 +355,31 @@ def tree_commit_raw(blocks: Sequence[tuple], n_leaves: int,
     _check(load().rcv_tree_commit(arr, len(blocks), n_leaves, len(out_ptrs),
                                   outs, acc_dtype, numel, float(divisor),
                                   variant, stream))
+
+
+class TreePlan:
+    """Prebuilt pointer arrays for repeated rcv_tree_commit_at calls: one
+    plan per (cover, outputs), then one cheap call per bucket or slice.
+    blocks = [(base_ptr, lo, level, dtype)], ascending lo; outs = [base_ptr]."""
+
+    def __init__(self, blocks: Sequence[tuple], n_leaves: int,
+                 outs: Sequence[int], acc_dtype: int, divisor: float,
+                 variant: int = VARIANT_AUTO):
+        self.n = len(blocks)
+        self.arr = (_Block * max(1, self.n))()
+        for i, (ptr, lo, level, dt) in enumerate(blocks):
+            self.arr[i] = _Block(ptr, lo, level, dt)
+        self.n_out = len(outs)
+        self.outs = (ctypes.c_void_p * max(1, self.n_out))(*outs)
+        self.n_leaves = n_leaves
+        self.acc = acc_dtype
+        self.divisor = float(divisor)
+        self.variant = variant
+        self.fn = load().rcv_tree_commit_at
+
+    def run(self, in_offset: int, out_offset: int, numel: int, stream: int) -> None:
+        if numel == 0 or self.n_out == 0:
+            return
+        _check(self.fn(self.arr, self.n, self.n_leaves, self.n_out, self.outs,
+                       self.acc, in_offset, out_offset, numel, self.divisor,
+                       self.variant, stream))

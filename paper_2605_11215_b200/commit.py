@@ -143,6 +143,7 @@ class GradientCommit:
         self.grads = {r: torch.empty(numel, dtype=dtype, device=self.placement[r])
                       for r in members}
         self._scratch: Dict[torch.device, List[torch.Tensor]] = {}
+        self._plan_cache = None
         # optional launch timing: list of (start_event, end_event, algo_bytes, kind)
         self.timing: Optional[list] = None
         _lib.enable_peer_access(sorted({d.index for d in self.placement.values()}))
@@ -157,85 +158,97 @@ class GradientCommit:
     def _end_of_step(self) -> None:
         """Hook run after the last bucket of a step is committed."""
 
-    def _scratch_buf(self, dev: torch.device, i: int, n: int) -> torch.Tensor:
+    def _scratch_buf(self, dev: torch.device, i: int) -> torch.Tensor:
+        """Full-length partial buffer i on dev (multi-device covers only):
+        bucket k's partial lives at the bucket's own offset, so partials and
+        leaves share one pointer offset per bucket."""
         pool = self._scratch.setdefault(dev, [])
-        maxlen = max(hi - lo for lo, hi in self.bounds)
         while len(pool) <= i:
-            pool.append(torch.empty(maxlen, dtype=torch.float32 if self.dtype == torch.bfloat16
+            pool.append(torch.empty(self.numel, dtype=torch.float32 if self.dtype == torch.bfloat16
                                     else self.dtype, device=dev))
-        return pool[i][:n]
+        return pool[i]
+
+    def _plan_for(self, leaves: Dict[int, Tuple[int, torch.Tensor]]):
+        """Launch plan of a leaf set (cached while the set is unchanged):
+        prebuilt pointer arrays, so each bucket is one or two cheap calls."""
+        members = tuple(self.comm.members)
+        cached = self._plan_cache
+        if cached is not None and cached[0] is leaves and cached[1] == members:
+            return cached[2]
+        b = self.state.b
+        acc = _lib.dtype_code(self.grads[members[0]])
+        outs = [self.grads[r] for r in members]
+        owner = {m: self.placement[rid] for m, (rid, _) in leaves.items()}
+        cover = block_cover(owner, b)
+        pre = []
+        if len(cover) == 1:
+            # every present leaf on one device: one fused launch per bucket
+            ins = [(leaves[m][1].data_ptr(), m, 0, _lib.dtype_code(leaves[m][1]))
+                   for m in sorted(leaves)]
+            top_dev = owner[min(leaves)]
+        else:
+            ins, used = [], {}
+            for blo, blev in cover:
+                span = [m for m in sorted(leaves) if blo <= m < blo + (1 << blev)]
+                dev = owner[span[0]]
+                if len(span) == 1:
+                    t = leaves[span[0]][1]
+                    ins.append((t.data_ptr(), blo, blev, _lib.dtype_code(t)))
+                    continue
+                buf = self._scratch_buf(dev, used.get(dev, 0))
+                used[dev] = used.get(dev, 0) + 1
+                sub = [(leaves[m][1].data_ptr(), m - blo, 0, _lib.dtype_code(leaves[m][1]))
+                       for m in span]
+                pre.append((dev, _lib.TreePlan(sub, 1 << blev, [buf.data_ptr()], acc, 0.0,
+                                               self.variant)))
+                ins.append((buf.data_ptr(), blo, blev, acc))
+            top_dev = self.placement[members[0]]
+        top = _lib.TreePlan(ins, b, [o.data_ptr() for o in outs], acc, float(b), self.variant)
+        others = sorted({o.device for o in outs} | {d for d, _ in pre} | set(owner.values()),
+                        key=lambda d: d.index)
+        plan = (pre, top, top_dev, [d for d in others if d != top_dev], len(ins), len(outs))
+        self._plan_cache = (leaves, members, plan)
+        return plan
 
     def _reduce_bucket(self, k: int, leaves: Dict[int, Tuple[int, torch.Tensor]]) -> int:
         """Commit bucket k from ``leaves`` {m: (rid, tensor)}; returns launches."""
         lo, hi = self.bounds[k]
         n = hi - lo
-        outs = [self.grads[r][lo:hi] for r in self.comm.members]
         if n == 0:
             return 0
-        b = self.state.b
         if not leaves:
-            for o in outs:
-                _lib.zero_(o)
-            return len(outs)
-        owner = {m: self.placement[rid] for m, (rid, _) in leaves.items()}
-        cover = block_cover(owner, b)
-        launches = 0
-        if len(cover) == 1:
-            # every present leaf on one device: one fused launch
-            blo, blev = cover[0]
-            ins = [(leaves[m][1][lo:hi], m, 0) for m in sorted(leaves)]
-            self._on_device(outs, owner[min(leaves)],
-                            lambda: self._timed(ins, outs, lambda: _lib.tree_commit(
-                                ins, b, outs, float(b), self.variant)))
-            return 1
-        # local partials per cover node, then the cross-device combine
-        parts = []
-        used: Dict[torch.device, int] = {}
-        for blo, blev in cover:
-            span = [m for m in sorted(leaves) if blo <= m < blo + (1 << blev)]
-            dev = owner[span[0]]
-            if len(span) == 1:
-                parts.append((leaves[span[0]][1][lo:hi], blo, blev))
-                continue
-            buf = self._scratch_buf(dev, used.get(dev, 0), n)
-            used[dev] = used.get(dev, 0) + 1
-            sub = [(leaves[m][1][lo:hi], m - blo, 0) for m in span]
-            with torch.cuda.device(dev):
-                _lib.tree_commit(sub, 1 << blev, [buf], 0.0, self.variant)
-            launches += 1
-            parts.append((buf, blo, blev))
-        combine_dev = self.placement[self.comm.members[0]]
-        self._on_device(outs, combine_dev,
-                        lambda: self._timed(parts, outs, lambda: _lib.tree_commit(
-                            parts, b, outs, float(b), self.variant)),
-                        extra=[p[0] for p in parts])
-        return launches + 1
+            for r in self.comm.members:
+                _lib.zero_(self.grads[r][lo:hi])
+            return len(self.comm.members)
+        pre, top, top_dev, others, n_in, n_out = self._plan_for(leaves)
+        for dev, tp in pre:
+            tp.run(lo, lo, n, torch.cuda.current_stream(dev).cuda_stream)
+        es = self.grads[self.comm.members[0]].element_size()
+        self._on_device(top_dev, others, lambda: self._timed(
+            (n_in + n_out) * n * es,
+            lambda: top.run(lo, lo, n, torch.cuda.current_stream(top_dev).cuda_stream)))
+        return len(pre) + 1
 
-    def _timed(self, ins, outs, launch):
+    def _timed(self, nbytes: int, launch) -> None:
         """Run a fused launch, bracketing it with CUDA events on its stream
-        when timing is on; algorithmic bytes = every input and output once."""
+        when timing is on; nbytes = every input and output once."""
         if self.timing is None:
             launch()
             return
-        nbytes = sum(t.numel() * t.element_size() for t, _, _ in ins) + \
-            sum(o.numel() * o.element_size() for o in outs)
         a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         launch()
         z.record()
         self.timing.append((a, z, nbytes, "fused", (0, 0)))
 
-    def _on_device(self, outs, dev, launch, extra=()):
+    def _on_device(self, dev, others, launch) -> None:
         """Run ``launch`` on dev's current stream, ordered after the other
         devices' streams (inputs / previous readers) and before them."""
-        devs = sorted({t.device for t in list(outs) + list(extra)} - {dev},
-                      key=lambda d: d.index)
-        if not devs:
-            with torch.cuda.device(dev):
-                launch()
+        if not others:
+            launch()
             return
         s = torch.cuda.current_stream(dev)
-        for d in devs:
+        for d in others:
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream(d))
             s.wait_event(ev)
@@ -243,7 +256,7 @@ class GradientCommit:
             launch()
         ev = torch.cuda.Event()
         ev.record(s)
-        for d in devs:
+        for d in others:
             torch.cuda.current_stream(d).wait_event(ev)
 
     # ---- one step (control flow of trainer.py:324-487) ----
@@ -335,13 +348,22 @@ class GradientCommit:
                 admitted[rid].append(nxt)
                 comm.contrib_boundary[rid] += 1
 
+        leaf_cache: list = [None, None]
+
         def collect() -> Dict[int, Tuple[int, torch.Tensor]]:
+            # the leaf set changes only when admissions, roles or membership
+            # do; reuse the dict (and with it the launch plan) otherwise
+            key = (comm.epoch, comm.boundary_latch,
+                   tuple((r, comm.roles[r], len(admitted.get(r, ()))) for r in comm.members))
+            if leaf_cache[0] == key:
+                return leaf_cache[1]
             lv: Dict[int, Tuple[int, torch.Tensor]] = {}
             for rid in comm.members:
                 if comm.roles[rid] in SPARE_ROLES and not comm.boundary_latch:
                     continue      # virtual zeroing: spare work never enters
                 for i in admitted.get(rid, ()):
                     lv[i] = (rid, leaf(i, rid) if self._holds(rid) else None)
+            leaf_cache[0], leaf_cache[1] = key, lv
             return lv
 
         def reduce(k: int) -> WorkResult:

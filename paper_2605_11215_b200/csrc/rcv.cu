@@ -1137,6 +1137,14 @@ int rcv_tree_program(const uint32_t *lo, const uint32_t *level, int n_blocks,
 int rcv_tree_commit(const rcv_block *blocks, int n_blocks, uint32_t n_leaves,
                     int n_out, void *const *out, int acc_dtype, size_t numel,
                     double divisor, int variant, void *stream) {
+  return rcv_tree_commit_at(blocks, n_blocks, n_leaves, n_out, out, acc_dtype, 0, 0,
+                            numel, divisor, variant, stream);
+}
+
+int rcv_tree_commit_at(const rcv_block *blocks, int n_blocks, uint32_t n_leaves,
+                       int n_out, void *const *out, int acc_dtype, size_t in_offset,
+                       size_t out_offset, size_t numel, double divisor, int variant,
+                       void *stream) {
   if (n_blocks < 0 || n_blocks > RCV_MAX_IN || n_out < 0 || n_out > RCV_MAX_OUT)
     return set_err(RCV_ERANGE, "block/output count out of range");
   uint32_t lo[RCV_MAX_IN], lev[RCV_MAX_IN];
@@ -1154,11 +1162,11 @@ int rcv_tree_commit(const rcv_block *blocks, int n_blocks, uint32_t n_leaves,
   for (int i = 0; i < n_blocks; ++i) {
     rc = check_dtype(acc_dtype, blocks[i].dtype);
     if (rc) return rc;
-    r.in[i] = (const char *)blocks[i].ptr;
+    r.in[i] = (const char *)blocks[i].ptr + in_offset * esize(blocks[i].dtype);
     r.in_dt[i] = blocks[i].dtype;
   }
   r.n_out = n_out;
-  for (int j = 0; j < n_out; ++j) r.out[j] = (char *)out[j];
+  for (int j = 0; j < n_out; ++j) r.out[j] = (char *)out[j] + out_offset * esize(acc_dtype);
   uint32_t L = 0;
   while ((1ull << L) < n_leaves) ++L;
   if (L <= 6) {  // compile-time tree kernels cover up to 64 leaves

@@ -141,6 +141,7 @@ class DistributedGradientCommit(GradientCommit):
         self._seq = 0
         self._calls = 0
         self._pending = None  # (lo, hi) of the last combined bucket to broadcast locally
+        self._plan_cache = None
         self.barriers = 0  # barrier kernels launched (for launch accounting)
         torch.cuda.synchronize(self.device)
         dist.barrier(group=group)
@@ -212,50 +213,68 @@ class DistributedGradientCommit(GradientCommit):
         z.record()
         self.timing.append((a, z, nbytes, kind, nvlink))
 
+    def _dist_plan(self, leaves):
+        """Per leaf set (cached): the local pre-reduce plans, the combine
+        plan over every cover node's pool slot, and NVLink byte counts."""
+        members = tuple(self.comm.members)
+        cached = self._plan_cache
+        if cached is not None and cached[0] is leaves and cached[1] == members:
+            return cached[2]
+        b = self.state.b
+        ranks = self._live_ranks()
+        owner = {m: self.rank_of[rid] for m, (rid, _) in leaves.items()}
+        cover, slot_of = plan_bucket(owner, b, ranks, self.pool_slots)
+        pre = []
+        for blo, blev in cover:
+            rk, j = slot_of[(blo, blev)]
+            if rk != self.rank:
+                continue
+            span = [m for m in sorted(leaves) if blo <= m < blo + (1 << blev)]
+            sub = [(leaves[m][1].data_ptr(), m - blo, 0, self._code) for m in span]
+            dst = self.pool_ptr[self.rank] + j * self.lmax * self._es
+            pre.append((_lib.TreePlan(sub, 1 << blev, [dst], self._code, 0.0, self.variant),
+                        len(sub)))
+        combine = None
+        if self.rank in ranks:
+            blocks = [(self.pool_ptr[rk] + j * self.lmax * self._es, blo, blev, self._code)
+                      for (blo, blev), (rk, j) in sorted(slot_of.items())]
+            prim = [self._primary(rk) for rk in ranks]
+            outs = [self.grad_ptr[r] for r in prim]
+            combine = (_lib.TreePlan(blocks, b, outs, self._code, float(b), self.combine_variant),
+                       sum(1 for rk, _ in slot_of.values() if rk != self.rank),
+                       sum(1 for r in prim if not self._holds(r)), len(blocks), len(outs))
+        plan = (pre, combine, ranks)
+        self._plan_cache = (leaves, members, plan)
+        return plan
+
     def _reduce_bucket(self, k: int, leaves) -> int:
         lo, hi = self.bounds[k]
         n = hi - lo
         if n == 0:
             return 0
-        members = list(self.comm.members)
-        b = self.state.b
         if not leaves:
-            for r in members:
+            for r in self.comm.members:
                 if self._holds(r):
                     _lib.zero_(self.grads[r][lo:hi])
             return 1
-        set_idx = self._calls % 2
+        pre, combine, ranks = self._dist_plan(leaves)
+        set_off = (self._calls % 2) * self.pool_slots * self.lmax
         self._calls += 1
-        owner = {m: self.rank_of[rid] for m, (rid, _) in leaves.items()}
-        cover, slot_of = plan_bucket(owner, b, self._live_ranks(), self.pool_slots)
-        launches = 0
-        for blo, blev in cover:
-            span = [m for m in sorted(leaves) if blo <= m < blo + (1 << blev)]
-            rk, j = slot_of[(blo, blev)]
-            if rk == self.rank:
-                dst = self.pool[(set_idx * self.pool_slots + j) * self.lmax:][:n]
-                ins = [(leaves[m][1][lo:hi], m - blo, 0) for m in span]
-                self._timed_launch("prereduce", (len(ins) + 1) * n * self._es,
-                                   lambda: _lib.tree_commit(ins, 1 << blev, [dst], 0.0,
-                                                            self.variant))
-                launches += 1
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        for tp, n_leaf in pre:
+            self._timed_launch("prereduce", (n_leaf + 1) * n * self._es,
+                               lambda: tp.run(lo, set_off, n, stream))
         self._barrier()
-        ranks = self._live_ranks()
-        if self.rank in ranks:
+        launches = len(pre)
+        if combine is not None:
+            tp, r_in, r_out, n_in, n_out = combine
             a, z = owner_slice(n, ranks.index(self.rank), len(ranks))
             if z > a:
-                blocks = [(self._pool_at(rk, set_idx, j, a), blo, blev, self._code)
-                          for (blo, blev), (rk, j) in sorted(slot_of.items())]
-                prim = [self._primary(rk) for rk in ranks]
-                outs = [self.grad_ptr[r] + (lo + a) * self._es for r in prim]
-                stream = torch.cuda.current_stream(self.device).cuda_stream
                 sl = (z - a) * self._es
-                remote_in = sum(1 for rk, _ in slot_of.values() if rk != self.rank)
-                remote_out = sum(1 for r in prim if not self._holds(r))
-                local = (len(blocks) - remote_in) + (len(outs) - remote_out)
-                self._timed_launch("combine", local * sl, lambda: _lib.tree_commit_raw(
-                    blocks, b, outs, z - a, self._code, float(b), stream,
-                    self.combine_variant), nvlink=(remote_in * sl, remote_out * sl))
+                local = (n_in - r_in) + (n_out - r_out)
+                self._timed_launch("combine", local * sl,
+                                   lambda: tp.run(set_off + a, lo + a, z - a, stream),
+                                   nvlink=(r_in * sl, r_out * sl))
                 launches += 1
         self._pending = (lo, hi)
         return launches
