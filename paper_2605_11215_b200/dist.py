@@ -142,6 +142,11 @@ class DistributedGradientCommit(GradientCommit):
         self._calls = 0
         self._pending = None  # (lo, hi) of the last combined bucket to broadcast locally
         self._plan_cache = None
+        # pre-reduce stream: bucket k+1's HBM-bound pre-reduce overlaps bucket
+        # k's NVLink-bound combine on the caller's stream
+        self.pstream = torch.cuda.Stream(self.device)
+        self._set_free = [None, None]   # event: pool set reusable (all peers done)
+        self._in_step = False
         self.barriers = 0  # barrier kernels launched (for launch accounting)
         torch.cuda.synchronize(self.device)
         dist.barrier(group=group)
@@ -190,6 +195,8 @@ class DistributedGradientCommit(GradientCommit):
 
     def _end_of_step(self) -> None:
         self._barrier()
+        self._in_step = False
+        self._set_free = [None, None]
 
     def check_peers(self) -> None:
         """Raise if any barrier so far timed out on a peer (reads the device
@@ -258,13 +265,30 @@ class DistributedGradientCommit(GradientCommit):
                     _lib.zero_(self.grads[r][lo:hi])
             return 1
         pre, combine, ranks = self._dist_plan(leaves)
-        set_off = (self._calls % 2) * self.pool_slots * self.lmax
+        sidx = self._calls % 2
+        set_off = sidx * self.pool_slots * self.lmax
         self._calls += 1
-        stream = torch.cuda.current_stream(self.device).cuda_stream
-        for tp, n_leaf in pre:
-            self._timed_launch("prereduce", (n_leaf + 1) * n * self._es,
-                               lambda: tp.run(lo, set_off, n, stream))
+        main = torch.cuda.current_stream(self.device)
+        stream = main.cuda_stream
+        if not self._in_step:
+            # the leaves were produced on the caller's stream
+            self._in_step = True
+            self.pstream.wait_stream(main)
+        if self._set_free[sidx] is not None:
+            self.pstream.wait_event(self._set_free[sidx])
+        with torch.cuda.stream(self.pstream):
+            for tp, n_leaf in pre:
+                self._timed_launch("prereduce", (n_leaf + 1) * n * self._es,
+                                   lambda: tp.run(lo, set_off, n, self.pstream.cuda_stream))
+        ready = torch.cuda.Event()
+        ready.record(self.pstream)
+        main.wait_event(ready)
         self._barrier()
+        # every live peer passed this barrier after its previous combine, so
+        # the other pool set (read by that combine) may be overwritten
+        free = torch.cuda.Event()
+        free.record(main)
+        self._set_free[1 - sidx] = free
         launches = len(pre)
         if combine is not None:
             tp, r_in, r_out, n_in, n_out = combine
