@@ -301,6 +301,7 @@ def run_ours(args):
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         start.record(stream)
+        t_host = time.perf_counter()
         for s in range(args.warmup, total_steps):
             kill.step = s
             a = torch.cuda.Event(enable_timing=True)
@@ -310,6 +311,7 @@ def run_ours(args):
             launches += out.launches
             step_ev.append(a)
         end.record(stream)
+        host_ms = (time.perf_counter() - t_host) * 1e3 / args.steps
         torch.cuda.synchronize()
     elapsed_ms = start.elapsed_time(end)
     if world > 1:
@@ -382,6 +384,7 @@ def run_ours(args):
         "step_ms": {"median": statistics.median(step_ms), "max": max(step_ms),
                     "failure_step": step_ms[fail_idx[0]] if fail_idx else None},
         "replica_agreement": agree,
+        "host_enqueue_ms_per_step": host_ms,
         "gpu_launches": launches + getattr(eng, "barriers", 0),
         "clocks": clk.summary(),
         "e2e": e2e,

@@ -189,8 +189,9 @@ class DistributedGradientCommit(GradientCommit):
         mask = 0
         for r in ranks:
             mask |= 1 << r
-        _lib.barrier(self.flags, self.flag_ptr, self.rank, mask, self._seq,
-                     self.timeout_ns, self.status)
+        self._timed_launch("barrier", 0, lambda: _lib.barrier(
+            self.flags, self.flag_ptr, self.rank, mask, self._seq,
+            self.timeout_ns, self.status))
         self._flush_broadcast()
 
     def _end_of_step(self) -> None:
