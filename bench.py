@@ -296,7 +296,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    eng.timing = []
+    eng.start_timing()
     with Clocks(local) as clk:
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
@@ -327,10 +327,11 @@ def run_ours(args):
     # roofline per kernel kind over the timed region (CUDA events on the
     # launching stream around every launch)
     kinds = {}
-    for a, z, nb, kind, (nin, nout) in eng.timing:
+    recs = eng.drain_timing()
+    for kind, ms, nb, nin, nout in recs:
         k = kinds.setdefault(kind, {"launches": 0, "ms": 0.0, "bytes": 0, "nvl_in": 0, "nvl_out": 0})
         k["launches"] += 1
-        k["ms"] += a.elapsed_time(z)
+        k["ms"] += ms
         k["bytes"] += nb
         k["nvl_in"] += nin
         k["nvl_out"] += nout
@@ -347,7 +348,6 @@ def run_ours(args):
     fail_idx = [i for i, o in enumerate(outcomes) if o.events]
     normal = [ms for i, ms in enumerate(step_ms) if i not in fail_idx]
     recovery_ms = (step_ms[fail_idx[0]] - statistics.median(normal)) if fail_idx and normal else None
-    eng.timing = None
 
     # correctness spot check inside the bench: every live replica holds the
     # same bytes (one kernel wrote them all)
@@ -385,7 +385,7 @@ def run_ours(args):
                     "failure_step": step_ms[fail_idx[0]] if fail_idx else None},
         "replica_agreement": agree,
         "host_enqueue_ms_per_step": host_ms,
-        "gpu_launches": launches + getattr(eng, "barriers", 0),
+        "gpu_launches": len(recs),
         "clocks": clk.summary(),
         "e2e": e2e,
     }

@@ -212,6 +212,59 @@ int rcv_barrier(uint64_t *local_flags, void *const *peer_flags, int n, int me,
                 uint64_t live_mask, uint64_t value, uint64_t timeout_ns,
                 uint32_t *status, void *stream);
 
+/* ---- native per-bucket runtime for the multi-process commit --------------
+ * One context per rank (flags, status, a side stream for pre-reduces, the
+ * barrier sequence, the pending local broadcast); one plan per leaf cover
+ * (prepared fold requests: validated once, relaunched per bucket).  A bucket
+ * then costs the host one call: rcv_plan_bucket enqueues
+ *   side stream: wait(pool set free) -> pre-reduce nodes -> record(ready)
+ *   main stream: wait(ready) -> barrier -> broadcast(previous bucket) ->
+ *                record(other set free) -> combine(owner slice)
+ * and rcv_ctx_finish closes the step (barrier + last broadcast). */
+typedef struct rcv_ctx rcv_ctx;
+typedef struct rcv_plan rcv_plan;
+
+int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags,
+                   void *const *peer_flags, uint32_t *status,
+                   uint64_t timeout_ns, rcv_ctx **out);
+int rcv_ctx_destroy(rcv_ctx *ctx);
+int rcv_ctx_finish(rcv_ctx *ctx, uint64_t live_mask, int participate,
+                   void *main_stream);
+int rcv_ctx_set_timing(rcv_ctx *ctx, int on);
+/* Drain recorded launch timings (call after synchronising): up to `max`
+ * entries of kind (0 pre-reduce, 1 barrier, 2 broadcast, 3 combine),
+ * milliseconds, algorithmic HBM bytes, NVLink in / out bytes. */
+int rcv_ctx_timing(rcv_ctx *ctx, int max, int *kind, float *ms, double *bytes,
+                   double *nvl_in, double *nvl_out, int *count);
+
+typedef struct {
+  int n_pre;                     /* local pre-reduce nodes */
+  const rcv_block *pre_blocks;   /* their leaves, concatenated */
+  const int *pre_counts;         /* leaves per node */
+  const uint32_t *pre_leaves;    /* canonical subtree size (2^level) per node */
+  void *const *pre_out;          /* pool slot of each node in set 0 */
+  size_t set_stride;             /* elements from pool set 0 to set 1 */
+  int n_comb;                    /* cover nodes (0: this rank takes no part) */
+  const rcv_block *comb_blocks;  /* every node's pool slot in set 0, ascending lo */
+  uint32_t n_leaves;             /* B */
+  int n_comb_out;
+  void *const *comb_out;         /* primary replica of every live rank */
+  int slice_q, slice_nr;         /* this rank's owner slice among the live ranks */
+  int n_bcast;
+  const void *bcast_src;         /* this rank's primary */
+  void *const *bcast_out;        /* this rank's other live replicas */
+  int acc_dtype;
+  double divisor;
+  int variant, comb_variant;
+  uint64_t live_mask;
+  int participate;
+  int remote_in, remote_out;     /* NVLink accounting of the combine */
+} rcv_plan_desc;
+
+int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *desc, rcv_plan **out);
+int rcv_plan_destroy(rcv_plan *plan);
+int rcv_plan_bucket(rcv_plan *plan, size_t lo, size_t n, void *main_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,6 +30,8 @@ EXPORTS = (
     "rcv_tree_program", "rcv_copy", "rcv_zero", "rcv_compare",
     "rcv_sgd_commit", "rcv_unit_lanes", "rcv_toy_grad",
     "rcv_ipc_export", "rcv_ipc_import", "rcv_barrier", "rcv_tree_commit_at",
+    "rcv_ctx_create", "rcv_ctx_destroy", "rcv_ctx_finish", "rcv_ctx_set_timing",
+    "rcv_ctx_timing", "rcv_plan_create", "rcv_plan_destroy", "rcv_plan_bucket",
 )
 
 
@@ -40,6 +42,26 @@ class RcvError(RuntimeError):
 class _Block(ctypes.Structure):
     _fields_ = [("ptr", ctypes.c_void_p), ("lo", ctypes.c_uint32),
                 ("level", ctypes.c_uint32), ("dtype", ctypes.c_int)]
+
+
+class PlanDesc(ctypes.Structure):
+    """rcv_plan_desc (include/rcv.h)."""
+    _fields_ = [
+        ("n_pre", ctypes.c_int), ("pre_blocks", ctypes.POINTER(_Block)),
+        ("pre_counts", ctypes.POINTER(ctypes.c_int)),
+        ("pre_leaves", ctypes.POINTER(ctypes.c_uint32)),
+        ("pre_out", ctypes.POINTER(ctypes.c_void_p)), ("set_stride", ctypes.c_size_t),
+        ("n_comb", ctypes.c_int), ("comb_blocks", ctypes.POINTER(_Block)),
+        ("n_leaves", ctypes.c_uint32), ("n_comb_out", ctypes.c_int),
+        ("comb_out", ctypes.POINTER(ctypes.c_void_p)),
+        ("slice_q", ctypes.c_int), ("slice_nr", ctypes.c_int),
+        ("n_bcast", ctypes.c_int), ("bcast_src", ctypes.c_void_p),
+        ("bcast_out", ctypes.POINTER(ctypes.c_void_p)),
+        ("acc_dtype", ctypes.c_int), ("divisor", ctypes.c_double),
+        ("variant", ctypes.c_int), ("comb_variant", ctypes.c_int),
+        ("live_mask", ctypes.c_uint64), ("participate", ctypes.c_int),
+        ("remote_in", ctypes.c_int), ("remote_out", ctypes.c_int),
+    ]
 
 
 _lib: Optional[ctypes.CDLL] = None
@@ -89,6 +111,16 @@ def load() -> ctypes.CDLL:
         "rcv_barrier": (i32, [vp, pvp, i32, i32, u64, u64, u64, vp, vp]),
         "rcv_tree_commit_at": (i32, [ctypes.POINTER(_Block), i32, u32, i32, pvp,
                                      i32, sz, sz, sz, ctypes.c_double, i32, vp]),
+        "rcv_ctx_create": (i32, [i32, i32, vp, pvp, vp, u64, ctypes.POINTER(vp)]),
+        "rcv_ctx_destroy": (i32, [vp]),
+        "rcv_ctx_finish": (i32, [vp, u64, i32, vp]),
+        "rcv_ctx_set_timing": (i32, [vp, i32]),
+        "rcv_ctx_timing": (i32, [vp, i32, ctypes.POINTER(i32), ctypes.POINTER(ctypes.c_float),
+                                 ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                 ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)]),
+        "rcv_plan_create": (i32, [vp, ctypes.POINTER(PlanDesc), ctypes.POINTER(vp)]),
+        "rcv_plan_destroy": (i32, [vp]),
+        "rcv_plan_bucket": (i32, [vp, sz, sz, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -383,3 +415,58 @@ class TreePlan:
         _check(self.fn(self.arr, self.n, self.n_leaves, self.n_out, self.outs,
                        self.acc, in_offset, out_offset, numel, self.divisor,
                        self.variant, stream))
+
+
+KIND_NAMES = ("prereduce", "barrier", "broadcast", "combine")
+
+
+class BucketRuntime:
+    """The native per-bucket runtime of one rank (rcv_ctx) and its current
+    plan (rcv_plan)."""
+
+    def __init__(self, n_ranks: int, me: int, flags: torch.Tensor,
+                 peer_flag_ptrs: Sequence[int], status: torch.Tensor,
+                 timeout_ns: int):
+        lib = load()
+        arr = (ctypes.c_void_p * n_ranks)(*peer_flag_ptrs)
+        h = ctypes.c_void_p(0)
+        _check(lib.rcv_ctx_create(n_ranks, me, flags.data_ptr(), arr,
+                                  status.data_ptr(), timeout_ns, ctypes.byref(h)))
+        self.ctx = h
+        self.plan = None
+        self._keep = None
+
+    def set_plan(self, desc: "PlanDesc", keep) -> None:
+        h = ctypes.c_void_p(0)
+        _check(load().rcv_plan_create(self.ctx, ctypes.byref(desc), ctypes.byref(h)))
+        if self.plan is not None:
+            load().rcv_plan_destroy(self.plan)
+        self.plan, self._keep = h, keep
+
+    def bucket(self, lo: int, n: int, stream: int) -> None:
+        _check(load().rcv_plan_bucket(self.plan, lo, n, stream))
+
+    def finish(self, live_mask: int, participate: bool, stream: int) -> None:
+        _check(load().rcv_ctx_finish(self.ctx, live_mask, int(participate), stream))
+
+    def set_timing(self, on: bool) -> None:
+        _check(load().rcv_ctx_set_timing(self.ctx, int(on)))
+
+    def timings(self, max_n: int = 1 << 16):
+        kind = (ctypes.c_int * max_n)()
+        ms = (ctypes.c_float * max_n)()
+        by = (ctypes.c_double * max_n)()
+        ni = (ctypes.c_double * max_n)()
+        no = (ctypes.c_double * max_n)()
+        cnt = ctypes.c_int(0)
+        _check(load().rcv_ctx_timing(self.ctx, max_n, kind, ms, by, ni, no, ctypes.byref(cnt)))
+        return [(KIND_NAMES[kind[i]], ms[i], by[i], ni[i], no[i]) for i in range(cnt.value)]
+
+    def close(self) -> None:
+        lib = load()
+        if self.plan is not None:
+            lib.rcv_plan_destroy(self.plan)
+            self.plan = None
+        if self.ctx:
+            lib.rcv_ctx_destroy(self.ctx)
+            self.ctx = None

@@ -241,6 +241,18 @@ class GradientCommit:
         z.record()
         self.timing.append((a, z, nbytes, "fused", (0, 0)))
 
+    def start_timing(self) -> None:
+        """Record every fused launch from now on (CUDA events on its stream)."""
+        self.timing = []
+
+    def drain_timing(self):
+        """[(kind, ms, hbm_bytes, nvlink_in, nvlink_out)] per launch since
+        start_timing (call after synchronising); stops recording."""
+        out = [(kind, a.elapsed_time(z), nb, nin, nout)
+               for a, z, nb, kind, (nin, nout) in (self.timing or [])]
+        self.timing = None
+        return out
+
     def _on_device(self, dev, others, launch) -> None:
         """Run ``launch`` on dev's current stream, ordered after the other
         devices' streams (inputs / previous readers) and before them."""

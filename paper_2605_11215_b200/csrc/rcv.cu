@@ -1141,10 +1141,34 @@ int rcv_tree_commit(const rcv_block *blocks, int n_blocks, uint32_t n_leaves,
                             numel, divisor, variant, stream);
 }
 
-int rcv_tree_commit_at(const rcv_block *blocks, int n_blocks, uint32_t n_leaves,
-                       int n_out, void *const *out, int acc_dtype, size_t in_offset,
-                       size_t out_offset, size_t numel, double divisor, int variant,
-                       void *stream) {
+}  // extern "C"
+
+namespace {
+// Validate a canonical-tree cover once and fill everything rcv_fold needs
+// (stack program, heap tables, perfect-tree shortcut); pointers unshifted.
+int prepare_tree(const rcv_block *blocks, int n_blocks, uint32_t n_leaves, int n_out,
+                 void *const *out, int acc_dtype, double divisor, FoldReq &r);
+
+void shift(FoldReq &r, size_t in_offset, size_t out_offset) {
+  for (int i = 0; i < r.n_in; ++i) r.in[i] += in_offset * esize(r.in_dt[i]);
+  for (int j = 0; j < r.n_out; ++j) r.out[j] += out_offset * esize(r.acc_dt);
+}
+}  // namespace
+
+extern "C" int rcv_tree_commit_at(const rcv_block *blocks, int n_blocks, uint32_t n_leaves,
+                                  int n_out, void *const *out, int acc_dtype, size_t in_offset,
+                                  size_t out_offset, size_t numel, double divisor, int variant,
+                                  void *stream) {
+  FoldReq r;
+  int rc = prepare_tree(blocks, n_blocks, n_leaves, n_out, out, acc_dtype, divisor, r);
+  if (rc) return rc;
+  shift(r, in_offset, out_offset);
+  return run_fold(r, numel, variant, (cudaStream_t)stream, current_device_sms());
+}
+
+namespace {
+int prepare_tree(const rcv_block *blocks, int n_blocks, uint32_t n_leaves, int n_out,
+                 void *const *out, int acc_dtype, double divisor, FoldReq &r) {
   if (n_blocks < 0 || n_blocks > RCV_MAX_IN || n_out < 0 || n_out > RCV_MAX_OUT)
     return set_err(RCV_ERANGE, "block/output count out of range");
   uint32_t lo[RCV_MAX_IN], lev[RCV_MAX_IN];
@@ -1152,7 +1176,7 @@ int rcv_tree_commit_at(const rcv_block *blocks, int n_blocks, uint32_t n_leaves,
     lo[i] = blocks[i].lo;
     lev[i] = blocks[i].level;
   }
-  FoldReq r;
+  r = FoldReq();
   int depth = 0;
   int rc = rcv_tree_program(lo, lev, n_blocks, n_leaves, r.op, &depth);
   if (rc) return rc;
@@ -1162,11 +1186,11 @@ int rcv_tree_commit_at(const rcv_block *blocks, int n_blocks, uint32_t n_leaves,
   for (int i = 0; i < n_blocks; ++i) {
     rc = check_dtype(acc_dtype, blocks[i].dtype);
     if (rc) return rc;
-    r.in[i] = (const char *)blocks[i].ptr + in_offset * esize(blocks[i].dtype);
+    r.in[i] = (const char *)blocks[i].ptr;
     r.in_dt[i] = blocks[i].dtype;
   }
   r.n_out = n_out;
-  for (int j = 0; j < n_out; ++j) r.out[j] = (char *)out[j] + out_offset * esize(acc_dtype);
+  for (int j = 0; j < n_out; ++j) r.out[j] = (char *)out[j];
   uint32_t L = 0;
   while ((1ull << L) < n_leaves) ++L;
   if (L <= 6) {  // compile-time tree kernels cover up to 64 leaves
@@ -1194,8 +1218,11 @@ int rcv_tree_commit_at(const rcv_block *blocks, int n_blocks, uint32_t n_leaves,
       r.full_L = fl;
     }
   }
-  return run_fold(r, numel, variant, (cudaStream_t)stream, current_device_sms());
+  return RCV_OK;
 }
+}  // namespace
+
+extern "C" {
 
 int rcv_ipc_export(const void *ptr, void *handle_out, size_t *offset_out) {
   void *base = nullptr;
@@ -1324,6 +1351,292 @@ int rcv_toy_grad(int kind_linear, const double *params, const double *lanes,
     const unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>((dim + 255) / 256, (unsigned long long)sms * 8));
     toy_grad_kernel<<<(unsigned)blocks, 256, 0, st>>>(kind_linear, lanes, dim, scal, grad);
     CK(cudaGetLastError());
+  }
+  return RCV_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// native per-bucket runtime (multi-process commit)
+
+}  // extern "C"
+
+struct TimingRec {
+  int kind;
+  double bytes, nin, nout;
+  cudaEvent_t a, b;
+};
+
+struct rcv_ctx {
+  int n_ranks = 0, me = 0, device = 0, sms = 148;
+  BarrierParams bar;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_main = nullptr, ev_ready = nullptr, ev_free[2] = {nullptr, nullptr};
+  bool free_valid[2] = {false, false};
+  bool in_step = false;
+  unsigned long long calls = 0, seq = 0;
+  bool pending = false;
+  FoldReq pending_req;
+  size_t pending_lo = 0, pending_n = 0;
+  int pending_variant = 0;
+  bool timing = false;
+  std::vector<TimingRec> recs;
+  std::vector<cudaEvent_t> spare_events;
+  cudaEvent_t ev() {
+    if (!spare_events.empty()) {
+      cudaEvent_t e = spare_events.back();
+      spare_events.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+struct rcv_plan {
+  rcv_ctx *ctx = nullptr;
+  std::vector<FoldReq> pre;
+  std::vector<int> pre_count;
+  size_t set_stride = 0;
+  bool has_comb = false;
+  FoldReq comb;
+  int slice_q = 0, slice_nr = 1;
+  bool has_bcast = false;
+  FoldReq bcast;
+  int variant = 0, comb_variant = 0;
+  uint64_t live_mask = 0;
+  bool participate = false;
+  int remote_in = 0, remote_out = 0;
+};
+
+namespace {
+
+template <typename F>
+int timed(rcv_ctx *c, cudaStream_t st, int kind, double bytes, double nin, double nout, F &&launch) {
+  if (!c->timing) return launch();
+  TimingRec r{kind, bytes, nin, nout, c->ev(), c->ev()};
+  CK(cudaEventRecord(r.a, st));
+  int rc = launch();
+  CK(cudaEventRecord(r.b, st));
+  c->recs.push_back(r);
+  return rc;
+}
+
+int ctx_barrier(rcv_ctx *c, uint64_t live, bool participate, cudaStream_t st) {
+  if (!participate || __builtin_popcountll(live) < 2) return RCV_OK;
+  c->bar.live = live;
+  c->bar.value = ++c->seq;
+  return timed(c, st, 1, 0, 0, 0, [&]() {
+    barrier_kernel<<<1, 32, 0, st>>>(c->bar);
+    CK(cudaGetLastError());
+    return RCV_OK;
+  });
+}
+
+int ctx_flush(rcv_ctx *c, cudaStream_t st) {
+  if (!c->pending) return RCV_OK;
+  c->pending = false;
+  FoldReq r = c->pending_req;
+  shift(r, c->pending_lo, c->pending_lo);
+  const double bytes = (double)(r.n_in + r.n_out) * c->pending_n * esize(r.acc_dt);
+  return timed(c, st, 2, bytes, 0, 0,
+               [&]() { return run_fold(r, c->pending_n, c->pending_variant, st, c->sms); });
+}
+
+}  // namespace
+
+extern "C" {
+
+int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer_flags,
+                   uint32_t *status, uint64_t timeout_ns, rcv_ctx **out) {
+  if (n_ranks < 1 || n_ranks > 32 || me < 0 || me >= n_ranks)
+    return set_err(RCV_ERANGE, "ctx: n_ranks %d me %d", n_ranks, me);
+  rcv_ctx *c = new rcv_ctx();
+  c->n_ranks = n_ranks;
+  c->me = me;
+  CK(cudaGetDevice(&c->device));
+  c->sms = dev_sms(c->device);
+  memset(&c->bar, 0, sizeof c->bar);
+  for (int r = 0; r < n_ranks; ++r) c->bar.peer[r] = (unsigned long long *)peer_flags[r];
+  c->bar.local = (unsigned long long *)local_flags;
+  c->bar.status = status;
+  c->bar.timeout_ns = timeout_ns;
+  c->bar.n = n_ranks;
+  c->bar.me = me;
+  CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_free[0], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_free[1], cudaEventDisableTiming));
+  *out = c;
+  return RCV_OK;
+}
+
+int rcv_ctx_destroy(rcv_ctx *c) {
+  if (!c) return RCV_OK;
+  cudaStreamSynchronize(c->side);
+  for (auto &r : c->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : c->spare_events) cudaEventDestroy(e);
+  cudaEventDestroy(c->ev_main);
+  cudaEventDestroy(c->ev_ready);
+  cudaEventDestroy(c->ev_free[0]);
+  cudaEventDestroy(c->ev_free[1]);
+  cudaStreamDestroy(c->side);
+  delete c;
+  return RCV_OK;
+}
+
+int rcv_ctx_set_timing(rcv_ctx *c, int on) {
+  c->timing = on != 0;
+  return RCV_OK;
+}
+
+int rcv_ctx_timing(rcv_ctx *c, int max, int *kind, float *ms, double *bytes, double *nvl_in,
+                   double *nvl_out, int *count) {
+  int n = 0;
+  for (auto &r : c->recs) {
+    if (n < max) {
+      kind[n] = r.kind;
+      CK(cudaEventElapsedTime(&ms[n], r.a, r.b));
+      bytes[n] = r.bytes;
+      nvl_in[n] = r.nin;
+      nvl_out[n] = r.nout;
+      ++n;
+    }
+    c->spare_events.push_back(r.a);
+    c->spare_events.push_back(r.b);
+  }
+  c->recs.clear();
+  *count = n;
+  return RCV_OK;
+}
+
+int rcv_ctx_finish(rcv_ctx *c, uint64_t live_mask, int participate, void *main_stream) {
+  cudaStream_t st = (cudaStream_t)main_stream;
+  int rc = ctx_barrier(c, live_mask, participate != 0, st);
+  if (rc) return rc;
+  rc = ctx_flush(c, st);
+  if (rc) return rc;
+  if (c->in_step) {
+    // the side stream's work is all upstream of main by now; make the next
+    // step's first pre-reduce wait for this step's tail
+    CK(cudaEventRecord(c->ev_main, st));
+  }
+  c->in_step = false;
+  c->free_valid[0] = c->free_valid[1] = false;
+  return RCV_OK;
+}
+
+int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
+  rcv_plan *p = new rcv_plan();
+  p->ctx = ctx;
+  p->set_stride = d->set_stride;
+  p->variant = d->variant;
+  p->comb_variant = d->comb_variant;
+  p->live_mask = d->live_mask;
+  p->participate = d->participate != 0;
+  p->remote_in = d->remote_in;
+  p->remote_out = d->remote_out;
+  int off = 0;
+  for (int i = 0; i < d->n_pre; ++i) {
+    FoldReq r;
+    void *dst = d->pre_out[i];
+    int rc = prepare_tree(d->pre_blocks + off, d->pre_counts[i], d->pre_leaves[i], 1, &dst,
+                          d->acc_dtype, 0.0, r);
+    if (rc) {
+      delete p;
+      return rc;
+    }
+    p->pre.push_back(r);
+    p->pre_count.push_back(d->pre_counts[i]);
+    off += d->pre_counts[i];
+  }
+  if (d->n_comb > 0 && d->participate) {
+    int rc = prepare_tree(d->comb_blocks, d->n_comb, d->n_leaves, d->n_comb_out, d->comb_out,
+                          d->acc_dtype, d->divisor, p->comb);
+    if (rc) {
+      delete p;
+      return rc;
+    }
+    p->has_comb = true;
+    p->slice_q = d->slice_q;
+    p->slice_nr = d->slice_nr;
+  }
+  if (d->n_bcast > 0) {
+    FoldReq &r = p->bcast;
+    r.n_in = 1;
+    r.in[0] = (const char *)d->bcast_src;
+    r.in_dt[0] = d->acc_dtype;
+    r.op[0] = 0;
+    r.n_out = d->n_bcast;
+    for (int j = 0; j < d->n_bcast; ++j) r.out[j] = (char *)d->bcast_out[j];
+    r.acc_dt = d->acc_dtype;
+    p->has_bcast = true;
+  }
+  *out = p;
+  return RCV_OK;
+}
+
+int rcv_plan_destroy(rcv_plan *p) {
+  delete p;
+  return RCV_OK;
+}
+
+int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
+  if (n == 0) return RCV_OK;
+  rcv_ctx *c = p->ctx;
+  cudaStream_t main = (cudaStream_t)main_stream;
+  const int es = esize(p->has_comb ? p->comb.acc_dt : RCV_F32);
+  if (!c->in_step) {
+    c->in_step = true;  // leaves were produced on the caller's stream
+    CK(cudaEventRecord(c->ev_main, main));
+    CK(cudaStreamWaitEvent(c->side, c->ev_main, 0));
+  }
+  const int sidx = (int)(c->calls++ % 2);
+  const size_t set_off = sidx * p->set_stride;
+  if (c->free_valid[sidx]) CK(cudaStreamWaitEvent(c->side, c->ev_free[sidx], 0));
+  for (size_t i = 0; i < p->pre.size(); ++i) {
+    FoldReq r = p->pre[i];
+    shift(r, lo, set_off);
+    const double bytes = (double)(p->pre_count[i] + 1) * n * esize(r.acc_dt);
+    int rc = timed(c, c->side, 0, bytes, 0, 0,
+                   [&]() { return run_fold(r, n, p->variant, c->side, c->sms); });
+    if (rc) return rc;
+  }
+  CK(cudaEventRecord(c->ev_ready, c->side));
+  CK(cudaStreamWaitEvent(main, c->ev_ready, 0));
+  int rc = ctx_barrier(c, p->live_mask, p->participate, main);
+  if (rc) return rc;
+  rc = ctx_flush(c, main);
+  if (rc) return rc;
+  // every live peer passed this barrier after its previous combine: the
+  // other pool set, which that combine read, may be overwritten
+  CK(cudaEventRecord(c->ev_free[1 - sidx], main));
+  c->free_valid[1 - sidx] = true;
+  if (p->has_comb) {
+    const size_t units = (n + 63) / 64;
+    const size_t a = std::min(n, units * p->slice_q / p->slice_nr * 64);
+    const size_t z = std::min(n, units * (p->slice_q + 1) / p->slice_nr * 64);
+    if (z > a) {
+      FoldReq r = p->comb;
+      shift(r, set_off + a, lo + a);
+      const double sl = (double)(z - a) * es;
+      const double local = (double)(r.n_in - p->remote_in + r.n_out - p->remote_out) * sl;
+      rc = timed(c, main, 3, local, p->remote_in * sl, p->remote_out * sl,
+                 [&]() { return run_fold(r, z - a, p->comb_variant, main, c->sms); });
+      if (rc) return rc;
+    }
+  }
+  if (p->has_bcast) {
+    c->pending = true;
+    c->pending_req = p->bcast;
+    c->pending_lo = lo;
+    c->pending_n = n;
+    c->pending_variant = p->variant;
   }
   return RCV_OK;
 }

@@ -23,14 +23,20 @@ crosses GPUs:
 
 Partial pools are double-buffered by call parity, so one barrier per bucket
 suffices (a rank passing barrier k+1 has finished combine k); one more
-barrier closes the step.  Dead replicas' microbatches are not in the cover,
-so their memory is never read; a rank whose replicas all died stops taking
-part in barriers and launches.
+barrier closes the step.  Pre-reduces run on a side stream, so bucket k+1's
+HBM-bound pre-reduce overlaps bucket k's NVLink-bound combine.  The whole
+per-bucket schedule lives in the native runtime (rcv_ctx / rcv_plan in
+librcv.so): a plan is prepared once per leaf cover and each bucket costs the
+host one call.  Dead replicas' microbatches are not in the cover, so their
+memory is never read; a rank whose replicas all died stops taking part in
+barriers and launches.
 """
 
 from __future__ import annotations
 
 from typing import Dict, List, Optional, Sequence
+
+import ctypes
 
 import torch
 import torch.distributed as dist
@@ -138,16 +144,9 @@ class DistributedGradientCommit(GradientCommit):
                          for r in members}
         self.pool_ptr = pb.share(self.pool)
         self.flag_ptr = pb.share(self.flags)
-        self._seq = 0
-        self._calls = 0
-        self._pending = None  # (lo, hi) of the last combined bucket to broadcast locally
-        self._plan_cache = None
-        # pre-reduce stream: bucket k+1's HBM-bound pre-reduce overlaps bucket
-        # k's NVLink-bound combine on the caller's stream
-        self.pstream = torch.cuda.Stream(self.device)
-        self._set_free = [None, None]   # event: pool set reusable (all peers done)
-        self._in_step = False
-        self.barriers = 0  # barrier kernels launched (for launch accounting)
+        self.rt = _lib.BucketRuntime(self.world, self.rank, self.flags, self.flag_ptr,
+                                     self.status, self.timeout_ns)
+        self._plan_key = None
         torch.cuda.synchronize(self.device)
         dist.barrier(group=group)
 
@@ -163,41 +162,17 @@ class DistributedGradientCommit(GradientCommit):
         """Lowest live replica on `rank`: the one the combine stores into."""
         return next((r for r in self.comm.members if self.rank_of[r] == rank), None)
 
-    def _flush_broadcast(self) -> None:
-        """Copy the last combined bucket from this rank's primary replica to
-        its other live replicas (HBM only).  Runs after a barrier, so every
-        peer's stores into the primary have landed."""
-        if self._pending is None:
-            return
-        lo, hi = self._pending
-        self._pending = None
-        mine = [r for r in self.comm.members if self._holds(r)]
-        if len(mine) < 2:
-            return
-        src = self.grads[mine[0]][lo:hi]
-        outs = [self.grads[r][lo:hi] for r in mine[1:]]
-        self._timed_launch("broadcast", (1 + len(outs)) * (hi - lo) * self._es,
-                           lambda: _lib.fold([src], [0], outs, variant=self.variant))
-
-    def _barrier(self) -> None:
+    def _live_mask(self):
         ranks = self._live_ranks()
-        if self.rank not in ranks or len(ranks) < 2:
-            self._flush_broadcast()
-            return
-        self._seq += 1
-        self.barriers += 1
         mask = 0
         for r in ranks:
             mask |= 1 << r
-        self._timed_launch("barrier", 0, lambda: _lib.barrier(
-            self.flags, self.flag_ptr, self.rank, mask, self._seq,
-            self.timeout_ns, self.status))
-        self._flush_broadcast()
+        return ranks, mask
 
     def _end_of_step(self) -> None:
-        self._barrier()
-        self._in_step = False
-        self._set_free = [None, None]
+        ranks, mask = self._live_mask()
+        self.rt.finish(mask, self.rank in ranks,
+                       torch.cuda.current_stream(self.device).cuda_stream)
 
     def check_peers(self) -> None:
         """Raise if any barrier so far timed out on a peer (reads the device
@@ -206,54 +181,62 @@ class DistributedGradientCommit(GradientCommit):
         if bad:
             raise RuntimeError("peer ranks timed out in the commit barrier: mask 0x%x" % bad)
 
-    def _pool_at(self, rank: int, set_idx: int, slot: int, elem: int) -> int:
-        return self.pool_ptr[rank] + ((set_idx * self.pool_slots + slot) * self.lmax + elem) * self._es
+    def start_timing(self) -> None:
+        self.rt.set_timing(True)
 
-    def _timed_launch(self, kind: str, nbytes: int, launch, nvlink=(0, 0)) -> None:
-        """Launch; with timing on, bracket it with CUDA events and record
-        its algorithmic HBM bytes and NVLink (in, out) bytes."""
-        if self.timing is None:
-            launch()
-            return
-        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        launch()
-        z.record()
-        self.timing.append((a, z, nbytes, kind, nvlink))
+    def drain_timing(self):
+        """[(kind, ms, hbm_bytes, nvlink_in, nvlink_out)] of every launch
+        since start_timing (call after synchronising)."""
+        out = self.rt.timings()
+        self.rt.set_timing(False)
+        return out
 
-    def _dist_plan(self, leaves):
-        """Per leaf set (cached): the local pre-reduce plans, the combine
-        plan over every cover node's pool slot, and NVLink byte counts."""
-        members = tuple(self.comm.members)
-        cached = self._plan_cache
-        if cached is not None and cached[0] is leaves and cached[1] == members:
-            return cached[2]
+    def _set_plan(self, leaves) -> None:
+        """Build the native plan of a leaf set: local pre-reduce nodes, the
+        combine over every cover node's pool slot, the local broadcast."""
         b = self.state.b
-        ranks = self._live_ranks()
+        ranks, mask = self._live_mask()
         owner = {m: self.rank_of[rid] for m, (rid, _) in leaves.items()}
         cover, slot_of = plan_bucket(owner, b, ranks, self.pool_slots)
-        pre = []
+        Block = _lib._Block
+        pre_blocks, pre_counts, pre_leaves, pre_out = [], [], [], []
         for blo, blev in cover:
             rk, j = slot_of[(blo, blev)]
             if rk != self.rank:
                 continue
             span = [m for m in sorted(leaves) if blo <= m < blo + (1 << blev)]
-            sub = [(leaves[m][1].data_ptr(), m - blo, 0, self._code) for m in span]
-            dst = self.pool_ptr[self.rank] + j * self.lmax * self._es
-            pre.append((_lib.TreePlan(sub, 1 << blev, [dst], self._code, 0.0, self.variant),
-                        len(sub)))
-        combine = None
-        if self.rank in ranks:
-            blocks = [(self.pool_ptr[rk] + j * self.lmax * self._es, blo, blev, self._code)
-                      for (blo, blev), (rk, j) in sorted(slot_of.items())]
-            prim = [self._primary(rk) for rk in ranks]
-            outs = [self.grad_ptr[r] for r in prim]
-            combine = (_lib.TreePlan(blocks, b, outs, self._code, float(b), self.combine_variant),
-                       sum(1 for rk, _ in slot_of.values() if rk != self.rank),
-                       sum(1 for r in prim if not self._holds(r)), len(blocks), len(outs))
-        plan = (pre, combine, ranks)
-        self._plan_cache = (leaves, members, plan)
-        return plan
+            pre_blocks += [Block(leaves[m][1].data_ptr(), m - blo, 0, self._code) for m in span]
+            pre_counts.append(len(span))
+            pre_leaves.append(1 << blev)
+            pre_out.append(self.pool_ptr[self.rank] + j * self.lmax * self._es)
+        comb = [Block(self.pool_ptr[rk] + j * self.lmax * self._es, blo, blev, self._code)
+                for (blo, blev), (rk, j) in sorted(slot_of.items())]
+        prim = [self._primary(rk) for rk in ranks]
+        mine = [r for r in self.comm.members if self._holds(r)]
+        part = self.rank in ranks
+
+        def arr(ctype, xs):
+            return (ctype * max(1, len(xs)))(*xs)
+        keep = dict(pre_blocks=arr(Block, pre_blocks), pre_counts=arr(ctypes.c_int, pre_counts),
+                    pre_leaves=arr(ctypes.c_uint32, pre_leaves),
+                    pre_out=arr(ctypes.c_void_p, pre_out), comb=arr(Block, comb),
+                    comb_out=arr(ctypes.c_void_p, [self.grad_ptr[r] for r in prim]),
+                    bcast_out=arr(ctypes.c_void_p, [self.grads[r].data_ptr() for r in mine[1:]]))
+        d = _lib.PlanDesc(
+            n_pre=len(pre_counts), pre_blocks=keep["pre_blocks"], pre_counts=keep["pre_counts"],
+            pre_leaves=keep["pre_leaves"], pre_out=keep["pre_out"],
+            set_stride=self.pool_slots * self.lmax,
+            n_comb=len(comb) if part else 0, comb_blocks=keep["comb"], n_leaves=b,
+            n_comb_out=len(prim), comb_out=keep["comb_out"],
+            slice_q=ranks.index(self.rank) if part else 0, slice_nr=len(ranks),
+            n_bcast=max(0, len(mine) - 1),
+            bcast_src=self.grads[mine[0]].data_ptr() if mine else None,
+            bcast_out=keep["bcast_out"], acc_dtype=self._code, divisor=float(b),
+            variant=self.variant, comb_variant=self.combine_variant,
+            live_mask=mask, participate=int(part),
+            remote_in=sum(1 for rk, _ in slot_of.values() if rk != self.rank),
+            remote_out=sum(1 for r in prim if not self._holds(r)))
+        self.rt.set_plan(d, keep)
 
     def _reduce_bucket(self, k: int, leaves) -> int:
         lo, hi = self.bounds[k]
@@ -265,41 +248,9 @@ class DistributedGradientCommit(GradientCommit):
                 if self._holds(r):
                     _lib.zero_(self.grads[r][lo:hi])
             return 1
-        pre, combine, ranks = self._dist_plan(leaves)
-        sidx = self._calls % 2
-        set_off = sidx * self.pool_slots * self.lmax
-        self._calls += 1
-        main = torch.cuda.current_stream(self.device)
-        stream = main.cuda_stream
-        if not self._in_step:
-            # the leaves were produced on the caller's stream
-            self._in_step = True
-            self.pstream.wait_stream(main)
-        if self._set_free[sidx] is not None:
-            self.pstream.wait_event(self._set_free[sidx])
-        with torch.cuda.stream(self.pstream):
-            for tp, n_leaf in pre:
-                self._timed_launch("prereduce", (n_leaf + 1) * n * self._es,
-                                   lambda: tp.run(lo, set_off, n, self.pstream.cuda_stream))
-        ready = torch.cuda.Event()
-        ready.record(self.pstream)
-        main.wait_event(ready)
-        self._barrier()
-        # every live peer passed this barrier after its previous combine, so
-        # the other pool set (read by that combine) may be overwritten
-        free = torch.cuda.Event()
-        free.record(main)
-        self._set_free[1 - sidx] = free
-        launches = len(pre)
-        if combine is not None:
-            tp, r_in, r_out, n_in, n_out = combine
-            a, z = owner_slice(n, ranks.index(self.rank), len(ranks))
-            if z > a:
-                sl = (z - a) * self._es
-                local = (n_in - r_in) + (n_out - r_out)
-                self._timed_launch("combine", local * sl,
-                                   lambda: tp.run(set_off + a, lo + a, z - a, stream),
-                                   nvlink=(r_in * sl, r_out * sl))
-                launches += 1
-        self._pending = (lo, hi)
-        return launches
+        key = (id(leaves), tuple(self.comm.members))
+        if self._plan_key is None or self._plan_key[0] != key or self._plan_key[1] is not leaves:
+            self._set_plan(leaves)
+            self._plan_key = (key, leaves)
+        self.rt.bucket(lo, n, torch.cuda.current_stream(self.device).cuda_stream)
+        return 1
