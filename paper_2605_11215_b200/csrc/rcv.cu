@@ -659,6 +659,7 @@ struct FoldReq {
   char *out[RCV_MAX_OUT];
   int acc_dt = RCV_F32;
   double divisor = 0.0;
+  int max_ctas = 0;  // > 0: cap on the grid, so concurrent kernels share SMs
   int tree_L = -1;  // >= 0: canonical tree tables below are valid
   int full_L = -1;  // >= 0: inputs are the 2^full_L leaves of a perfect tree
   int8_t node_in[2 * RCV_MAX_IN - 1];
@@ -748,7 +749,8 @@ int launch_direct_p(const FoldReq &r, unsigned long long e0, unsigned long long 
   FoldParams p;
   fill_vec_params<A>(p, r, e0, nvec);
   const unsigned long long want = (nvec + 255) / 256;
-  const unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)sms * 8));
+  unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)sms * 8));
+  if (r.max_ctas > 0) blocks = std::min<unsigned long long>(blocks, (unsigned long long)r.max_ctas * 4);
   fold_direct_kernel<A, Prog><<<(unsigned)blocks, 256, 0, st>>>(p);
   CK(cudaGetLastError());
   return RCV_OK;
@@ -797,11 +799,26 @@ int launch_tma_p(const FoldReq &r, const TmaGeom &g, unsigned long long e0,
   p.stages = g.stages;
   p.vpt = g.vpt;
   auto kern = fold_tma_kernel<A, Prog>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+  {
+    // one attribute call per (kernel, device, size): it is not free
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const void *, int>, size_t>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    bool have = false;
+    for (auto &e : done)
+      if (e.first.first == (const void *)kern && e.first.second == dev && e.second >= g.smem) have = true;
+    if (!have) {
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 1024));
+      done.push_back({{(const void *)kern, dev}, 200 * 1024 + 1024});
+    }
+  }
   const unsigned long long tv = (unsigned long long)TMA_CONSUMERS * g.vpt;
   const unsigned long long ntiles = (nvec + tv - 1) / tv;
-  const unsigned long long blocks = std::max<unsigned long long>(
+  unsigned long long blocks = std::max<unsigned long long>(
       1, std::min<unsigned long long>(ntiles, (unsigned long long)sms * g.ctas_per_sm));
+  if (r.max_ctas > 0) blocks = std::min<unsigned long long>(blocks, (unsigned long long)r.max_ctas);
   kern<<<(unsigned)blocks, TMA_THREADS, g.smem, st>>>(p);
   CK(cudaGetLastError());
   return RCV_OK;
@@ -1531,6 +1548,14 @@ int rcv_ctx_finish(rcv_ctx *c, uint64_t live_mask, int participate, void *main_s
   return RCV_OK;
 }
 
+static int env_ctas(const char *name, int sms, double dflt_frac) {
+  const char *v = getenv(name);
+  const double f = v ? atof(v) : dflt_frac;
+  if (f <= 0) return 0;                    // 0: uncapped
+  if (f > 2.0) return (int)f;              // an absolute CTA count
+  return std::max(1, (int)(f * sms));      // a fraction of the SMs
+}
+
 int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
   rcv_plan *p = new rcv_plan();
   p->ctx = ctx;
@@ -1551,6 +1576,7 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       delete p;
       return rc;
     }
+    r.max_ctas = env_ctas("RCV_PRE_CTAS", ctx->sms, 0.0);
     p->pre.push_back(r);
     p->pre_count.push_back(d->pre_counts[i]);
     off += d->pre_counts[i];
@@ -1562,6 +1588,7 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       delete p;
       return rc;
     }
+    p->comb.max_ctas = env_ctas("RCV_COMB_CTAS", ctx->sms, 0.0);
     p->has_comb = true;
     p->slice_q = d->slice_q;
     p->slice_nr = d->slice_nr;
@@ -1575,6 +1602,7 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
     r.n_out = d->n_bcast;
     for (int j = 0; j < d->n_bcast; ++j) r.out[j] = (char *)d->bcast_out[j];
     r.acc_dt = d->acc_dtype;
+    r.max_ctas = env_ctas("RCV_BCAST_CTAS", ctx->sms, 0.0);
     p->has_bcast = true;
   }
   *out = p;
