@@ -12,7 +12,7 @@ for cfg in "$@"; do
     --gpus $N --steps 30 --warmup 5 --skip-cpu --e2e-steps 0 > $OUT/sweep_$i.json 2>/dev/null
   python3 -c "
 import json,sys
-d=json.load(open('$OUT/sweep_$i.json'))
+d=json.loads([l for l in open('$OUT/sweep_$i.json') if l.startswith('{')][-1])
 k=d['kernels']
 print('cfg=[$cfg] ms/step %.3f' % d['ms_per_step'], ' '.join('%s:%.0fus' % (n, v['mean_launch_us']) for n, v in k.items()), 'comb nvl in/out %.0f/%.0f' % (k['combine']['nvlink_in_gbs'], k['combine']['nvlink_out_gbs']))
 " || echo "cfg=[$cfg] failed"
