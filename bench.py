@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sample", type=int, default=1 << 23)
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--trace", default="", help="torch.profiler chrome trace prefix (diagnostics)")
     return ap.parse_args()
 
 
@@ -296,6 +297,18 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
+    if args.trace:
+        # diagnostics only: a CUPTI timeline of a few steps, then exit
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+            for s in range(args.warmup, args.warmup + 4):
+                kill.step = -1
+                eng.step(s, leaf, kill)
+            torch.cuda.synchronize()
+        prof.export_chrome_trace("%s_rank%d.json" % (args.trace, rank))
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
     eng.start_timing()
     with Clocks(local) as clk:
         start = torch.cuda.Event(enable_timing=True)
