@@ -59,6 +59,9 @@ extern "C" {
 
 const char *rcv_last_error(void);
 int rcv_version(void);
+/* Number of kernels this library has launched in this process (the bench's
+ * gpu_launches is the difference across its timed region). */
+unsigned long long rcv_launch_count(void);
 
 /* Number of CUDA devices visible (0 without a GPU; never fails on CPU). */
 int rcv_device_count(int *n);

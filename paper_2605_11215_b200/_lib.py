@@ -24,7 +24,7 @@ LIB_PATH = os.path.join(_HERE, "librcv.so")
 
 # every symbol include/rcv.h declares (tests check the export table)
 EXPORTS = (
-    "rcv_last_error", "rcv_version", "rcv_device_count",
+    "rcv_last_error", "rcv_version", "rcv_launch_count", "rcv_device_count",
     "rcv_enable_peer_access", "rcv_fold", "rcv_masked_allreduce",
     "rcv_masked_allreduce_multidev", "rcv_accumulate", "rcv_tree_commit",
     "rcv_tree_program", "rcv_copy", "rcv_zero", "rcv_compare",
@@ -82,6 +82,7 @@ def load() -> ctypes.CDLL:
     sig = {
         "rcv_last_error": (ctypes.c_char_p, []),
         "rcv_version": (i32, []),
+        "rcv_launch_count": (ctypes.c_ulonglong, []),
         "rcv_device_count": (i32, [ctypes.POINTER(i32)]),
         "rcv_enable_peer_access": (i32, [i32, ctypes.POINTER(i32)]),
         "rcv_fold": (i32, [i32, pvp, ctypes.POINTER(ctypes.c_uint8),
@@ -470,3 +471,8 @@ class BucketRuntime:
         if self.ctx:
             lib.rcv_ctx_destroy(self.ctx)
             self.ctx = None
+
+
+def launch_count() -> int:
+    """Kernels launched by librcv.so so far in this process."""
+    return int(load().rcv_launch_count())

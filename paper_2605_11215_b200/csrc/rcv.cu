@@ -34,6 +34,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -46,6 +47,7 @@
 // errors
 
 static thread_local std::string g_err;
+static std::atomic<unsigned long long> g_launches{0};  // kernels launched by this library
 
 static int set_err(int code, const char *fmt, ...) {
   char buf[512];
@@ -707,6 +709,7 @@ int launch_scalar_t(const FoldReq &r, unsigned long long e0, unsigned long long 
   p.numel = n;
   p.divisor = r.divisor;
   const unsigned long long blocks = std::min<unsigned long long>((n + 255) / 256, (unsigned long long)sms * 8);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   fold_scalar_kernel<A, MAXD><<<(unsigned)std::max<unsigned long long>(blocks, 1), 256, 0, st>>>(p);
   CK(cudaGetLastError());
   return RCV_OK;
@@ -751,6 +754,7 @@ int launch_direct_p(const FoldReq &r, unsigned long long e0, unsigned long long 
   const unsigned long long want = (nvec + 255) / 256;
   unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)sms * 8));
   if (r.max_ctas > 0) blocks = std::min<unsigned long long>(blocks, (unsigned long long)r.max_ctas * 4);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   fold_direct_kernel<A, Prog><<<(unsigned)blocks, 256, 0, st>>>(p);
   CK(cudaGetLastError());
   return RCV_OK;
@@ -819,6 +823,7 @@ int launch_tma_p(const FoldReq &r, const TmaGeom &g, unsigned long long e0,
   unsigned long long blocks = std::max<unsigned long long>(
       1, std::min<unsigned long long>(ntiles, (unsigned long long)sms * g.ctas_per_sm));
   if (r.max_ctas > 0) blocks = std::min<unsigned long long>(blocks, (unsigned long long)r.max_ctas);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   kern<<<(unsigned)blocks, TMA_THREADS, g.smem, st>>>(p);
   CK(cudaGetLastError());
   return RCV_OK;
@@ -968,6 +973,7 @@ struct TreeBuild {
 extern "C" {
 
 const char *rcv_last_error(void) { return g_err.c_str(); }
+unsigned long long rcv_launch_count(void) { return g_launches.load(); }
 int rcv_version(void) { return RCV_VERSION; }
 
 int rcv_device_count(int *n) {
@@ -1301,6 +1307,7 @@ int rcv_barrier(uint64_t *local_flags, void *const *peer_flags, int n, int me,
   p.timeout_ns = timeout_ns;
   p.n = n;
   p.me = me;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
   CK(cudaGetLastError());
   return RCV_OK;
@@ -1325,6 +1332,7 @@ int rcv_compare(const void *a, const void *b, size_t bytes,
   const int tail = (int)(bytes % 4);
   const int sms = current_device_sms();
   const unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>((nw + 255) / 256, (unsigned long long)sms * 8));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   compare_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
       (const uint32_t *)a, (const uint32_t *)b, nw, (const uint8_t *)a + nw * 4,
       (const uint8_t *)b + nw * 4, tail, d_count);
@@ -1337,12 +1345,12 @@ int rcv_sgd_commit(void *params, const void *flat, int dtype, size_t numel,
   if (!numel) return RCV_OK;
   const int sms = current_device_sms();
   const unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>((numel + 255) / 256, (unsigned long long)sms * 8));
+  if (dtype != RCV_F64 && dtype != RCV_F32) return set_err(RCV_EINVAL, "sgd dtype %d", dtype);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   if (dtype == RCV_F64)
     sgd_kernel<double><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>((double *)params, (const double *)flat, numel, b, lr);
-  else if (dtype == RCV_F32)
-    sgd_kernel<float><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>((float *)params, (const float *)flat, numel, b, lr);
   else
-    return set_err(RCV_EINVAL, "sgd dtype %d", dtype);
+    sgd_kernel<float><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>((float *)params, (const float *)flat, numel, b, lr);
   CK(cudaGetLastError());
   return RCV_OK;
 }
@@ -1352,6 +1360,7 @@ int rcv_unit_lanes(double *out, uint64_t base, size_t n, double scale,
   if (!n) return RCV_OK;
   const int sms = current_device_sms();
   const unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>((n + 255) / 256, (unsigned long long)sms * 8));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   unit_lanes_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(out, base, n, scale, shift, floor7);
   CK(cudaGetLastError());
   return RCV_OK;
@@ -1361,11 +1370,13 @@ int rcv_toy_grad(int kind_linear, const double *params, const double *lanes,
                  const double *wstar, size_t dim, double *grad, double *scal,
                  void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   toy_dot_kernel<<<1, TOY_T, 0, st>>>(kind_linear, params, lanes, wstar, dim, scal);
   CK(cudaGetLastError());
   if (dim && grad) {  // grad == NULL: loss only (the constant stream's x is g0)
     const int sms = current_device_sms();
     const unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>((dim + 255) / 256, (unsigned long long)sms * 8));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     toy_grad_kernel<<<(unsigned)blocks, 256, 0, st>>>(kind_linear, lanes, dim, scal, grad);
     CK(cudaGetLastError());
   }
@@ -1388,14 +1399,15 @@ struct rcv_ctx {
   int n_ranks = 0, me = 0, device = 0, sms = 148;
   BarrierParams bar;
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_main = nullptr, ev_ready = nullptr, ev_free[2] = {nullptr, nullptr};
-  bool free_valid[2] = {false, false};
+  cudaEvent_t ev_main = nullptr, ev_ready = nullptr, ev_arrived = nullptr;
   bool in_step = false;
   unsigned long long calls = 0, seq = 0;
-  bool pending = false;
-  FoldReq pending_req;
-  size_t pending_lo = 0, pending_n = 0;
-  int pending_variant = 0;
+  struct Pending {
+    FoldReq req;
+    size_t lo, n;
+    int variant;
+  };
+  std::vector<Pending> pending;  // combined buckets awaiting the local broadcast
   bool timing = false;
   std::vector<TimingRec> recs;
   std::vector<cudaEvent_t> spare_events;
@@ -1445,20 +1457,28 @@ int ctx_barrier(rcv_ctx *c, uint64_t live, bool participate, cudaStream_t st) {
   c->bar.live = live;
   c->bar.value = ++c->seq;
   return timed(c, st, 1, 0, 0, 0, [&]() {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     barrier_kernel<<<1, 32, 0, st>>>(c->bar);
     CK(cudaGetLastError());
     return RCV_OK;
   });
 }
 
-int ctx_flush(rcv_ctx *c, cudaStream_t st) {
-  if (!c->pending) return RCV_OK;
-  c->pending = false;
-  FoldReq r = c->pending_req;
-  shift(r, c->pending_lo, c->pending_lo);
-  const double bytes = (double)(r.n_in + r.n_out) * c->pending_n * esize(r.acc_dt);
-  return timed(c, st, 2, bytes, 0, 0,
-               [&]() { return run_fold(r, c->pending_n, c->pending_variant, st, c->sms); });
+// Broadcast the oldest `count` pending buckets (all of them when count < 0)
+// from this rank's primary replica to its other replicas, on stream st.
+int ctx_flush(rcv_ctx *c, cudaStream_t st, int count) {
+  int done = 0;
+  while (!c->pending.empty() && (count < 0 || done < count)) {
+    rcv_ctx::Pending e = c->pending.front();
+    c->pending.erase(c->pending.begin());
+    shift(e.req, e.lo, e.lo);
+    const double bytes = (double)(e.req.n_in + e.req.n_out) * e.n * esize(e.req.acc_dt);
+    int rc = timed(c, st, 2, bytes, 0, 0,
+                   [&]() { return run_fold(e.req, e.n, e.variant, st, c->sms); });
+    if (rc) return rc;
+    ++done;
+  }
+  return RCV_OK;
 }
 
 }  // namespace
@@ -1484,8 +1504,7 @@ int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&c->ev_free[0], cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&c->ev_free[1], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_arrived, cudaEventDisableTiming));
   *out = c;
   return RCV_OK;
 }
@@ -1500,8 +1519,7 @@ int rcv_ctx_destroy(rcv_ctx *c) {
   for (auto e : c->spare_events) cudaEventDestroy(e);
   cudaEventDestroy(c->ev_main);
   cudaEventDestroy(c->ev_ready);
-  cudaEventDestroy(c->ev_free[0]);
-  cudaEventDestroy(c->ev_free[1]);
+  cudaEventDestroy(c->ev_arrived);
   cudaStreamDestroy(c->side);
   delete c;
   return RCV_OK;
@@ -1534,17 +1552,16 @@ int rcv_ctx_timing(rcv_ctx *c, int max, int *kind, float *ms, double *bytes, dou
 
 int rcv_ctx_finish(rcv_ctx *c, uint64_t live_mask, int participate, void *main_stream) {
   cudaStream_t st = (cudaStream_t)main_stream;
+  if (c->in_step) {
+    // the side stream's tail (broadcasts) joins the caller's stream
+    CK(cudaEventRecord(c->ev_ready, c->side));
+    CK(cudaStreamWaitEvent(st, c->ev_ready, 0));
+  }
   int rc = ctx_barrier(c, live_mask, participate != 0, st);
   if (rc) return rc;
-  rc = ctx_flush(c, st);
+  rc = ctx_flush(c, st, -1);
   if (rc) return rc;
-  if (c->in_step) {
-    // the side stream's work is all upstream of main by now; make the next
-    // step's first pre-reduce wait for this step's tail
-    CK(cudaEventRecord(c->ev_main, st));
-  }
   c->in_step = false;
-  c->free_valid[0] = c->free_valid[1] = false;
   return RCV_OK;
 }
 
@@ -1626,7 +1643,18 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
   }
   const int sidx = (int)(c->calls++ % 2);
   const size_t set_off = sidx * p->set_stride;
-  if (c->free_valid[sidx]) CK(cudaStreamWaitEvent(c->side, c->ev_free[sidx], 0));
+  if (c->calls > 1) {
+    // ev_arrived marks the previous bucket's barrier: every peer had
+    // finished the combine before it (so this pool set, read by that
+    // combine's predecessor, is free) and every bucket before the previous
+    // one is complete in this rank's primary -> broadcast those here, off
+    // the main stream's critical path
+    CK(cudaStreamWaitEvent(c->side, c->ev_arrived, 0));
+    if (c->pending.size() > 1) {
+      int rc = ctx_flush(c, c->side, (int)c->pending.size() - 1);
+      if (rc) return rc;
+    }
+  }
   for (size_t i = 0; i < p->pre.size(); ++i) {
     FoldReq r = p->pre[i];
     shift(r, lo, set_off);
@@ -1639,12 +1667,7 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
   CK(cudaStreamWaitEvent(main, c->ev_ready, 0));
   int rc = ctx_barrier(c, p->live_mask, p->participate, main);
   if (rc) return rc;
-  rc = ctx_flush(c, main);
-  if (rc) return rc;
-  // every live peer passed this barrier after its previous combine: the
-  // other pool set, which that combine read, may be overwritten
-  CK(cudaEventRecord(c->ev_free[1 - sidx], main));
-  c->free_valid[1 - sidx] = true;
+  CK(cudaEventRecord(c->ev_arrived, main));
   if (p->has_comb) {
     const size_t units = (n + 63) / 64;
     const size_t a = std::min(n, units * p->slice_q / p->slice_nr * 64);
@@ -1659,13 +1682,7 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
       if (rc) return rc;
     }
   }
-  if (p->has_bcast) {
-    c->pending = true;
-    c->pending_req = p->bcast;
-    c->pending_lo = lo;
-    c->pending_n = n;
-    c->pending_variant = p->variant;
-  }
+  if (p->has_bcast) c->pending.push_back({p->bcast, lo, n, p->variant});
   return RCV_OK;
 }
 
