@@ -411,7 +411,8 @@ def run_ours(args):
         "allreduce_algbw_gbs": numel * 4 / (elapsed_ms / args.steps / 1e3) / 1e9,
         "recovery_ms": recovery_ms,
         "step_ms": {"median": statistics.median(step_ms), "max": max(step_ms),
-                    "failure_step": step_ms[fail_idx[0]] if fail_idx else None},
+                    "failure_step": step_ms[fail_idx[0]] if fail_idx else None,
+                    "all": [round(x, 3) for x in step_ms]},
         "replica_agreement": agree,
         "host_enqueue_ms_per_step": host_ms,
         "gpu_launches": n_launch,
