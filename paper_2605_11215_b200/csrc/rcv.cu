@@ -1399,13 +1399,14 @@ struct rcv_ctx {
   int n_ranks = 0, me = 0, device = 0, sms = 148;
   BarrierParams bar;
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_main = nullptr, ev_ready = nullptr, ev_arrived = nullptr;
+  cudaEvent_t ev_main = nullptr, ev_ready = nullptr, ev_arrived[3] = {nullptr, nullptr, nullptr};
   bool in_step = false;
   unsigned long long calls = 0, seq = 0;
   struct Pending {
     FoldReq req;
     size_t lo, n;
     int variant;
+    unsigned long long call;  // bucket call index that combined it
   };
   std::vector<Pending> pending;  // combined buckets awaiting the local broadcast
   bool timing = false;
@@ -1464,11 +1465,10 @@ int ctx_barrier(rcv_ctx *c, uint64_t live, bool participate, cudaStream_t st) {
   });
 }
 
-// Broadcast the oldest `count` pending buckets (all of them when count < 0)
-// from this rank's primary replica to its other replicas, on stream st.
-int ctx_flush(rcv_ctx *c, cudaStream_t st, int count) {
-  int done = 0;
-  while (!c->pending.empty() && (count < 0 || done < count)) {
+// Broadcast the pending buckets combined at call index <= upto (all of them
+// when upto < 0) from this rank's primary replica to its other replicas.
+int ctx_flush(rcv_ctx *c, cudaStream_t st, long long upto) {
+  while (!c->pending.empty() && (upto < 0 || (long long)c->pending.front().call <= upto)) {
     rcv_ctx::Pending e = c->pending.front();
     c->pending.erase(c->pending.begin());
     shift(e.req, e.lo, e.lo);
@@ -1476,7 +1476,6 @@ int ctx_flush(rcv_ctx *c, cudaStream_t st, int count) {
     int rc = timed(c, st, 2, bytes, 0, 0,
                    [&]() { return run_fold(e.req, e.n, e.variant, st, c->sms); });
     if (rc) return rc;
-    ++done;
   }
   return RCV_OK;
 }
@@ -1504,7 +1503,7 @@ int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&c->ev_arrived, cudaEventDisableTiming));
+  for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->ev_arrived[i], cudaEventDisableTiming));
   *out = c;
   return RCV_OK;
 }
@@ -1519,7 +1518,7 @@ int rcv_ctx_destroy(rcv_ctx *c) {
   for (auto e : c->spare_events) cudaEventDestroy(e);
   cudaEventDestroy(c->ev_main);
   cudaEventDestroy(c->ev_ready);
-  cudaEventDestroy(c->ev_arrived);
+  for (int i = 0; i < 3; ++i) cudaEventDestroy(c->ev_arrived[i]);
   cudaStreamDestroy(c->side);
   delete c;
   return RCV_OK;
@@ -1641,17 +1640,18 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
     CK(cudaEventRecord(c->ev_main, main));
     CK(cudaStreamWaitEvent(c->side, c->ev_main, 0));
   }
-  const int sidx = (int)(c->calls++ % 2);
-  const size_t set_off = sidx * p->set_stride;
-  if (c->calls > 1) {
-    // ev_arrived marks the previous bucket's barrier: every peer had
-    // finished the combine before it (so this pool set, read by that
-    // combine's predecessor, is free) and every bucket before the previous
-    // one is complete in this rank's primary -> broadcast those here, off
-    // the main stream's critical path
-    CK(cudaStreamWaitEvent(c->side, c->ev_arrived, 0));
-    if (c->pending.size() > 1) {
-      int rc = ctx_flush(c, c->side, (int)c->pending.size() - 1);
+  // Three pool sets: call j's pre-reduce overwrites the set last read by the
+  // combine of call j-3, which every peer finished before its barrier of
+  // call j-2.  So the side stream only waits for that barrier and can run
+  // up to two buckets ahead of the combines; the buckets combined at calls
+  // <= j-3 are then also complete in this rank's primary, and their local
+  // broadcasts go here, off the main stream.
+  const unsigned long long j = c->calls++;
+  const size_t set_off = (j % 3) * p->set_stride;
+  if (j >= 2) {
+    CK(cudaStreamWaitEvent(c->side, c->ev_arrived[(j - 2) % 3], 0));
+    if (j >= 3) {
+      int rc = ctx_flush(c, c->side, (long long)j - 3);
       if (rc) return rc;
     }
   }
@@ -1667,7 +1667,7 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
   CK(cudaStreamWaitEvent(main, c->ev_ready, 0));
   int rc = ctx_barrier(c, p->live_mask, p->participate, main);
   if (rc) return rc;
-  CK(cudaEventRecord(c->ev_arrived, main));
+  CK(cudaEventRecord(c->ev_arrived[j % 3], main));
   if (p->has_comb) {
     const size_t units = (n + 63) / 64;
     const size_t a = std::min(n, units * p->slice_q / p->slice_nr * 64);
@@ -1682,7 +1682,7 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
       if (rc) return rc;
     }
   }
-  if (p->has_bcast) c->pending.push_back({p->bcast, lo, n, p->variant});
+  if (p->has_bcast) c->pending.push_back({p->bcast, lo, n, p->variant, j});
   return RCV_OK;
 }
 

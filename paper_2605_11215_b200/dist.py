@@ -21,9 +21,10 @@ crosses GPUs:
    from its primary replica into its other replicas (HBM), so NVLink carries
    one copy per rank, not one per replica.
 
-Partial pools are double-buffered by call parity, so one barrier per bucket
-suffices (a rank passing barrier k+1 has finished combine k); one more
-barrier closes the step.  Pre-reduces run on a side stream, so bucket k+1's
+Partial pools are triple-buffered by call index, so one barrier per bucket
+suffices (a rank passing barrier k+1 has finished combine k) and the
+pre-reduce stream may run two buckets ahead; one more barrier closes the
+step.  Pre-reduces run on a side stream, so bucket k+1's
 HBM-bound pre-reduce overlaps bucket k's NVLink-bound combine.  The whole
 per-bucket schedule lives in the native runtime (rcv_ctx / rcv_plan in
 librcv.so): a plan is prepared once per leaf cover and each bucket costs the
@@ -134,7 +135,7 @@ class DistributedGradientCommit(GradientCommit):
         self.grads = {r: store[i * numel:(i + 1) * numel] for i, r in enumerate(local)}
         self.lmax = max(hi - lo for lo, hi in self.bounds)
         self.pool_slots = pool_slots
-        self.pool = torch.empty(2 * pool_slots * self.lmax, dtype=dtype, device=self.device)
+        self.pool = torch.empty(3 * pool_slots * self.lmax, dtype=dtype, device=self.device)
         self.flags = torch.zeros(64, dtype=torch.int64, device=self.device)
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.timeout_ns = int(barrier_timeout_s * 1e9)
