@@ -10,6 +10,9 @@ import json
 import os
 import sys
 
+# deterministic cuBLAS for the trajectory tests; must precede CUDA init
+os.environ.setdefault("CUBLAS_WORKSPACE_CONFIG", ":4096:8")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

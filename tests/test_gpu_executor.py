@@ -1,0 +1,70 @@
+"""North-star trajectory claim: a tiny transformer trained data-parallel
+through the canonical commit has a loss and parameter trajectory under
+failures that is bitwise the failure-free one (BASELINE configs[0] and a
+short configs[4]: successive failures 8 -> 4 replicas)."""
+
+import pytest
+import torch
+
+from paper_2605_11215_b200.executor import (CanonicalExecutor, TinyTransformer,
+                                            lm_loss, synthetic_lm_batch)
+
+pytestmark = pytest.mark.gpu
+
+
+class Schedule:
+    """{step: [(phase, bucket, [rids])]}, each entry fired once."""
+
+    def __init__(self, plan):
+        self.plan = {t: list(v) for t, v in plan.items()}
+        self.t = -1
+
+    def fire(self, phase, bucket=None):
+        cur = self.plan.get(self.t, [])
+        hit = [e for e in cur if e[0] == phase and (phase != "during_sync" or e[1] == bucket)]
+        self.plan[self.t] = [e for e in cur if e not in hit]
+        return [r for e in hit for r in e[2]]
+
+
+def train(w, g, k, steps, plan=None, seed=0):
+    torch.use_deterministic_algorithms(True)
+    torch.manual_seed(seed)
+    model = TinyTransformer(layers=2, d=64, heads=4, seq=32)
+    ex = CanonicalExecutor(model, synthetic_lm_batch(seed, micro=2, seq=32), lm_loss,
+                           w, g, k, lr=0.1)
+    sched = Schedule(plan or {})
+    losses, outs = [], []
+    for t in range(steps):
+        sched.t = t
+        out, loss = ex.step(t, sched)
+        losses.append(loss)
+        outs.append(out)
+    torch.cuda.synchronize()
+    return losses, ex.flat.clone(), outs, ex
+
+
+def test_tiny_transformer_one_replica_lost_bitwise():
+    """configs[0]: 4 replicas x 8 microbatches, one replica lost mid-iteration."""
+    ref_l, ref_p, _, _ = train(4, 8, 4, 5)
+    l, p, outs, ex = train(4, 8, 4, 5, {2: [("during_sync", 2, [1])]})
+    assert ref_l == l                         # every loss, bit for bit
+    assert torch.equal(ref_p, p)              # parameters after the last step
+    assert ref_l[-1] < ref_l[0]               # and it is learning
+    ev = outs[2].events[0]
+    assert ev["contrib"] == 24 and ev["g_ext"] == 3 and ev["n_bdry"] == 1
+    # replica 1's 8 microbatches were recomputed by survivors, nothing else
+    redo = [(m, rid) for t, m, rid in ex.computed if t == 2][32:]
+    assert sorted(m for m, _ in redo) == list(range(8, 16))
+    assert all(rid != 1 for _, rid in redo)
+
+
+def test_successive_failures_8_to_4_bitwise():
+    """configs[4] in miniature: 8 -> 4 replicas, deaths at every location."""
+    plan = {1: [("during_sync", 1, [3])], 3: [("before_sync", None, [6])],
+            4: [("after_sync", None, [0])], 6: [("during_sync", 0, [5])]}
+    ref_l, ref_p, _, _ = train(8, 4, 3, 8)
+    l, p, outs, _ = train(8, 4, 3, 8, plan)
+    assert ref_l == l
+    assert torch.equal(ref_p, p)
+    assert outs[-1].w_cur == 4
+    assert all(o.contrib_total == 32 for o in outs)
