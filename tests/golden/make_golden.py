@@ -207,12 +207,62 @@ def fold_vectors():
     return cases
 
 
+def metrics_runs():
+    """sim.run_experiment metrics/v1 rows (sim.py:323-348, 363-413) for
+    schedules generated by the reference's own generator, plus the
+    acceptance gate's golden trace and throughput configs
+    (test_acceptance.py:339-375, 506-541)."""
+    from steadybatch.sim import (CostModel, ExperimentConfig, FailureSchedule,
+                                 GenerationSpec, InjectionPoint, ScheduleEntry,
+                                 generate_schedule, run_experiment)
+    runs = []
+
+    def add(name, cfg, sched):
+        res = run_experiment(cfg, sched)
+        runs.append(dict(
+            name=name,
+            config=dict(w_init=cfg.w_init, g_init=cfg.g_init, iterations=cfg.iterations,
+                        k_buckets=cfg.k_buckets, dim=cfg.dim, model_kind=cfg.model_kind,
+                        stream_seed=cfg.stream_seed, lr=cfg.lr, policy=cfg.policy),
+            entries=[[e.step, e.replica, e.location.serialize()] for e in sched.entries],
+            rows=res.rows, aborted=res.aborted))
+
+    add("appendix_e_golden_trace",
+        ExperimentConfig(w_init=32, g_init=8, iterations=4, k_buckets=4, dim=4,
+                         model_kind="constant", stream_seed=7, policy="static"),
+        FailureSchedule(GenerationSpec(32, 8, 4, 0, 2, 1, 3),
+                        [ScheduleEntry(1, 5, 0, InjectionPoint("during_sync", 1)),
+                         ScheduleEntry(2, 29, 3, InjectionPoint("during_sync", 0))]))
+    add("throughput_amortization",
+        ExperimentConfig(w_init=8, g_init=4, iterations=18, k_buckets=4, dim=3,
+                         model_kind="constant", stream_seed=3, policy="static",
+                         cost=CostModel(0.01, 0.5, 0.05, 0.003)),
+        FailureSchedule(GenerationSpec(8, 8, 4, 0, 2, 3, 10),
+                        [ScheduleEntry(3, 5, 0, InjectionPoint("before_sync")),
+                         ScheduleEntry(9, 2, 0, InjectionPoint("before_sync"))]))
+    rng = random.Random(7)
+    for j in range(10):
+        w = rng.randint(3, 12)
+        k = rng.randint(1, 4)
+        spec = GenerationSpec(w_init=w, ranks_per_replica=8, k_buckets=k,
+                              seed=rng.randrange(2 ** 31), count=rng.randint(1, min(w - 1, 4)),
+                              step_lo=0, step_hi=6, weights=(1.0, 2.0, 1.0))
+        cfg = ExperimentConfig(w_init=w, g_init=rng.randint(1, 6), iterations=6, k_buckets=k,
+                               dim=rng.randint(2, 5),
+                               model_kind=rng.choice(("constant", "linear")),
+                               stream_seed=rng.randrange(2 ** 31),
+                               policy=rng.choice(("static", "static", "adaptive")))
+        add("generated_%d" % j, cfg, generate_schedule(spec))
+    return runs
+
+
 def main():
     sys.path.insert(0, REF)
     import steadybatch as sb
     doc = {"generated_by": "tests/golden/make_golden.py",
            "reference": REF, "numpy": np.__version__,
-           "scenarios": [], "fold_vectors": fold_vectors()}
+           "scenarios": [], "fold_vectors": fold_vectors(),
+           "metrics_runs": metrics_runs()}
     for spec in scripted_scenarios() + random_scenarios():
         doc["scenarios"].append(dict(spec, rows=run_reference(sb, spec)))
     path = os.path.join(HERE, "scenarios.json")
