@@ -206,7 +206,8 @@ class DistributedGradientCommit(GradientCommit):
             if rk != self.rank:
                 continue
             span = [m for m in sorted(leaves) if blo <= m < blo + (1 << blev)]
-            pre_blocks += [Block(leaves[m][1].data_ptr(), m - blo, 0, self._code) for m in span]
+            pre_blocks += [Block(leaves[m][1].data_ptr(), m - blo, 0,
+                                 _lib.dtype_code(leaves[m][1])) for m in span]
             pre_counts.append(len(span))
             pre_leaves.append(1 << blev)
             pre_out.append(self.pool_ptr[self.rank] + j * self.lmax * self._es)
@@ -255,3 +256,45 @@ class DistributedGradientCommit(GradientCommit):
             self._plan_key = (key, leaves)
         self.rt.bucket(lo, n, torch.cuda.current_stream(self.device).cuda_stream)
         return 1
+
+
+def shard_bounds(numel: int, shards: int, align: int = 64):
+    """Contiguous shard ranges of a flat gradient, cuts on align elements."""
+    base = (numel // shards) // align * align
+    return [(i * base, numel if i == shards - 1 else (i + 1) * base) for i in range(shards)]
+
+
+class HSDPCommit:
+    """Hybrid-sharded data parallel: every replica spans `shards` GPUs (the
+    intra-replica shard group, where FSDP reduce-scatters each microbatch's
+    gradient), and the fault-tolerant canonical commit runs per shard
+    position over the replicate group of that position (PAPER.md:677-691:
+    ULFM on replicate_pg, NCCL on shard_pg).  A replica is atomic: a death
+    removes it from every shard position's group at the same logical point,
+    because every rank replays the same schedule.
+
+    Global rank = replica * shards + shard.  leaf(m, rid) returns this
+    rank's shard of microbatch m's gradient (bf16 or fp32; accumulation is
+    fp32)."""
+
+    def __init__(self, numel: int, shards: int, w_init: int, g_init: int,
+                 k_buckets: int, spares: int = 0, **kw):
+        rank, world = dist.get_rank(), dist.get_world_size()
+        n_rep = w_init + spares
+        if world != shards * n_rep:
+            raise ValueError("world %d != %d shards x %d replicas" % (world, shards, n_rep))
+        self.shards = shards
+        self.replica, self.shard = divmod(rank, shards)
+        groups = [dist.new_group([r * shards + s for r in range(n_rep)]) for s in range(shards)]
+        self.bounds = shard_bounds(numel, shards)
+        lo, hi = self.bounds[self.shard]
+        self.engine = DistributedGradientCommit(hi - lo, w_init, g_init, k_buckets,
+                                                group=groups[self.shard], spares=spares, **kw)
+
+    @property
+    def grad(self) -> torch.Tensor:
+        """This rank's committed shard gradient (its replica's)."""
+        return self.engine.grads[self.replica]
+
+    def step(self, t: int, leaf, injector=None):
+        return self.engine.step(t, leaf, injector)

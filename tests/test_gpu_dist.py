@@ -76,3 +76,73 @@ def test_distributed_commit_bitwise(combine_variant):
     assert res[0] == res[world - 1]
     # after replica 3 died: advanced 7-replica layout, G = 5 and a minor at 2
     assert res[0][2][2] == [(0, 5), (1, 5), (2, 5), (4, 5), (5, 5), (6, 5), (7, 2)]
+
+
+def _hsdp_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        from paper_2605_11215_b200.dist import HSDPCommit
+        from oracle import fold
+        shards, reps, g = 2, world // 2, 8
+        b = reps * g
+        numel = 2 * 4 * 64 * 21 + 64
+        hsdp = HSDPCommit(numel, shards, reps, g, 4)
+        lo, hi = hsdp.bounds[hsdp.shard]
+        full = [np.random.default_rng(500 + m).standard_normal(numel).astype(np.float32)
+                for m in range(b)]
+        # bf16 microbatch gradients (the FSDP reduce-scatter output), fp32 commit
+        bf = [torch.from_numpy(x).to(torch.bfloat16) for x in full]
+        mine = [t[lo:hi].contiguous().cuda() for t in bf]
+        widened = {m: t[lo:hi].float().numpy() for m, t in enumerate(bf)}
+        want = fold.canonical_tree(widened, b) / np.float32(b)
+
+        class Kill:
+            def __init__(self, plan):
+                self.plan = list(plan)
+
+            def fire(self, phase, bucket=None):
+                hit = [e for e in self.plan if e[0] == phase and (phase != "during_sync" or e[1] == bucket)]
+                self.plan = [e for e in self.plan if e not in hit]
+                return [r for e in hit for r in e[2]]
+
+        res = []
+        for t, plan in enumerate([[], [("during_sync", 1, [reps - 1])], []]):
+            out = hsdp.step(t, lambda m, rid: mine[m], Kill(plan))
+            torch.cuda.synchronize()
+            ok = (hsdp.replica not in hsdp.engine.comm.members or
+                  hsdp.grad.cpu().numpy().tobytes() == want.tobytes())
+            res.append((ok, out.contrib_total, out.w_cur))
+        q.put((rank, res))
+    except Exception as exc:
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_hsdp_commit_bf16_bitwise():
+    world = torch.cuda.device_count()
+    if world < 4:
+        pytest.skip("HSDP needs 2 shards x 2 replicas = 4 GPUs")
+    world = 4
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = torch.multiprocessing.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_hsdp_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert not isinstance(res[r], str), res[r]
+        assert all(ok for ok, _, _ in res[r]), res[r]
+        assert [tot for _, tot, _ in res[r]] == [16, 16, 16]
+        assert [w for _, _, w in res[r]] == [2, 1, 1]
