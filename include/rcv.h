@@ -205,11 +205,21 @@ int rcv_ipc_export(const void *ptr, void *handle_out, size_t *offset_out);
  * pointer to base + offset in this process. */
 int rcv_ipc_import(const void *handle, size_t offset, void **ptr_out);
 
+/* cuMem VMM shareable allocation (real-kill mode): `bytes` of device memory
+ * on the current GPU, mapped for every GPU that can reach it, exported as a
+ * POSIX file descriptor.  Importers hold a reference to the physical memory,
+ * so a peer's buffers stay valid after the peer process dies. */
+int rcv_vmm_alloc(size_t bytes, void **ptr_out, size_t *size_out, int *fd_out);
+/* Map a peer's exported allocation (fd already duplicated into this process,
+ * e.g. with pidfd_getfd); owner_device is the GPU holding the memory. */
+int rcv_vmm_import(int fd, size_t size, int owner_device, void **ptr_out);
+
 /* Cross-GPU barrier among the ranks in live_mask: rank `me` stores `value`
  * into slot `me` of every live peer's flag array (peer_flags[r], mapped
  * pointers), then waits until its own local_flags[r] >= value for every live
  * peer r, each wait bounded by timeout_ns of %globaltimer.  A peer that times
- * out sets bit r in *status (device uint32) instead of blocking forever.
+ * out sets bit r in *status (device uint32) instead of blocking forever;
+ * a peer whose bit is already set is neither signalled nor awaited again. 
  * Launched on `stream`, ordered after the caller's prior work. */
 int rcv_barrier(uint64_t *local_flags, void *const *peer_flags, int n, int me,
                 uint64_t live_mask, uint64_t value, uint64_t timeout_ns,
@@ -262,6 +272,8 @@ typedef struct {
   uint64_t live_mask;
   int participate;
   int remote_in, remote_out;     /* NVLink accounting of the combine */
+  int guarded;                   /* real-kill mode: skip the combine once a
+                                    live peer timed out (status word) */
 } rcv_plan_desc;
 
 int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *desc, rcv_plan **out);

@@ -32,6 +32,7 @@ EXPORTS = (
     "rcv_ipc_export", "rcv_ipc_import", "rcv_barrier", "rcv_tree_commit_at",
     "rcv_ctx_create", "rcv_ctx_destroy", "rcv_ctx_finish", "rcv_ctx_set_timing",
     "rcv_ctx_timing", "rcv_plan_create", "rcv_plan_destroy", "rcv_plan_bucket",
+    "rcv_vmm_alloc", "rcv_vmm_import",
 )
 
 
@@ -61,6 +62,7 @@ class PlanDesc(ctypes.Structure):
         ("variant", ctypes.c_int), ("comb_variant", ctypes.c_int),
         ("live_mask", ctypes.c_uint64), ("participate", ctypes.c_int),
         ("remote_in", ctypes.c_int), ("remote_out", ctypes.c_int),
+        ("guarded", ctypes.c_int),
     ]
 
 
@@ -122,6 +124,8 @@ def load() -> ctypes.CDLL:
         "rcv_plan_create": (i32, [vp, ctypes.POINTER(PlanDesc), ctypes.POINTER(vp)]),
         "rcv_plan_destroy": (i32, [vp]),
         "rcv_plan_bucket": (i32, [vp, sz, sz, vp]),
+        "rcv_vmm_alloc": (i32, [sz, ctypes.POINTER(vp), ctypes.POINTER(sz), ctypes.POINTER(i32)]),
+        "rcv_vmm_import": (i32, [i32, sz, i32, ctypes.POINTER(vp)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -476,3 +480,35 @@ class BucketRuntime:
 def launch_count() -> int:
     """Kernels launched by librcv.so so far in this process."""
     return int(load().rcv_launch_count())
+
+
+# ---- VMM shareable memory (real-kill mode) -----------------------------------
+
+def vmm_alloc(nbytes: int):
+    """(device ptr, mapped size, exported POSIX fd) on the current GPU."""
+    ptr, size, fd = ctypes.c_void_p(0), ctypes.c_size_t(0), ctypes.c_int(-1)
+    _check(load().rcv_vmm_alloc(nbytes, ctypes.byref(ptr), ctypes.byref(size), ctypes.byref(fd)))
+    return ptr.value, size.value, fd.value
+
+
+def vmm_import(fd: int, size: int, owner_device: int) -> int:
+    ptr = ctypes.c_void_p(0)
+    _check(load().rcv_vmm_import(fd, size, owner_device, ctypes.byref(ptr)))
+    return ptr.value
+
+
+class _CudaArray:
+    """__cuda_array_interface__ over raw device memory (for torch.as_tensor)."""
+
+    def __init__(self, ptr: int, numel: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (numel,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 2,
+                                         "strides": None}
+
+
+def tensor_at(ptr: int, numel: int, dtype: torch.dtype, device) -> torch.Tensor:
+    """A torch view of `numel` elements at device address ptr (no copy)."""
+    typestr = {torch.float32: "<f4", torch.float64: "<f8", torch.int64: "<i8",
+               torch.int32: "<i4"}[dtype]
+    with torch.cuda.device(device):
+        return torch.as_tensor(_CudaArray(ptr, numel, typestr), device=device)

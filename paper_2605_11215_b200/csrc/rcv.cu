@@ -197,6 +197,9 @@ struct FoldParams {
   uint32_t stage_bytes;     // TMA
   int stages;               // TMA
   int vpt;                  // TMA: vectors per consumer thread per input
+  // real-kill mode: skip the whole launch when a live peer has timed out
+  const unsigned int *guard;  // device status word (NULL: unguarded)
+  unsigned int guard_mask;    // the peers this launch reads
   // canonical tree (ProgTree): heap-indexed nodes, id = 2^(L-level)-1+idx
   int8_t node_in[2 * RCV_MAX_IN - 1];    // input feeding the node, or -1
   uint8_t present[2 * RCV_MAX_IN - 1];   // subtree holds at least one input
@@ -291,6 +294,7 @@ template <typename A, typename Prog>
 __global__ void __launch_bounds__(256)
     fold_direct_kernel(const __grid_constant__ FoldParams p) {
   using V = typename VecT<A>::V;
+  if (p.guard && (*p.guard & p.guard_mask)) return;
   for (unsigned long long v = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
        v < p.nvec; v += (unsigned long long)gridDim.x * blockDim.x) {
     auto ld = [&](int i) {
@@ -352,6 +356,7 @@ template <typename A, typename Prog>
 __global__ void __launch_bounds__(TMA_THREADS)
     fold_tma_kernel(const __grid_constant__ FoldParams p) {
   using V = typename VecT<A>::V;
+  if (p.guard && (*p.guard & p.guard_mask)) return;  // uniform: before any barrier
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)p.stages * p.stage_bytes);
   uint64_t *empty = full + p.stages;
@@ -436,6 +441,8 @@ struct ScalarParams {
   int n_out;
   unsigned long long numel;
   double divisor;
+  const unsigned int *guard;
+  unsigned int guard_mask;
 };
 
 template <typename A>
@@ -459,6 +466,7 @@ __device__ __forceinline__ double sdiv(double a, double d) { return __ddiv_rn(a,
 template <typename A, int MAXD>
 __global__ void __launch_bounds__(256)
     fold_scalar_kernel(const __grid_constant__ ScalarParams p) {
+  if (p.guard && (*p.guard & p.guard_mask)) return;
   for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
        e < p.numel; e += (unsigned long long)gridDim.x * blockDim.x) {
     A s[MAXD];
@@ -603,7 +611,9 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   const int t = threadIdx.x;
-  const bool peer = t < p.n && t != p.me && ((p.live >> t) & 1ull);
+  // a peer that already timed out is dead: never signal or wait on it again
+  const unsigned int dead = *(volatile const unsigned int *)p.status;
+  const bool peer = t < p.n && t != p.me && ((p.live >> t) & 1ull) && !((dead >> t) & 1u);
   // everything this GPU wrote before this kernel (partials, remote stores)
   // is made visible system-wide before the flag store releases it
   __threadfence_system();
@@ -662,6 +672,8 @@ struct FoldReq {
   int acc_dt = RCV_F32;
   double divisor = 0.0;
   int max_ctas = 0;  // > 0: cap on the grid, so concurrent kernels share SMs
+  const unsigned int *guard = nullptr;
+  unsigned int guard_mask = 0;
   int tree_L = -1;  // >= 0: canonical tree tables below are valid
   int full_L = -1;  // >= 0: inputs are the 2^full_L leaves of a perfect tree
   int8_t node_in[2 * RCV_MAX_IN - 1];
@@ -708,6 +720,8 @@ int launch_scalar_t(const FoldReq &r, unsigned long long e0, unsigned long long 
   for (int j = 0; j < r.n_out; ++j) p.out[j] = r.out[j] + e0 * sizeof(A);
   p.numel = n;
   p.divisor = r.divisor;
+  p.guard = r.guard;
+  p.guard_mask = r.guard_mask;
   const unsigned long long blocks = std::min<unsigned long long>((n + 255) / 256, (unsigned long long)sms * 8);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   fold_scalar_kernel<A, MAXD><<<(unsigned)std::max<unsigned long long>(blocks, 1), 256, 0, st>>>(p);
@@ -739,6 +753,8 @@ void fill_vec_params(FoldParams &p, const FoldReq &r, unsigned long long e0,
   for (int j = 0; j < r.n_out; ++j) p.out[j] = r.out[j] + e0 * sizeof(A);
   p.nvec = nvec;
   p.divisor = r.divisor;
+  p.guard = r.guard;
+  p.guard_mask = r.guard_mask;
   if (r.tree_L >= 0) {
     const int nodes = (2 << r.tree_L) - 1;
     memcpy(p.node_in, r.node_in, nodes);
@@ -1274,6 +1290,109 @@ int rcv_ipc_export(const void *ptr, void *handle_out, size_t *offset_out) {
   return RCV_OK;
 }
 
+// ---- cuMem VMM shareable allocations (real-kill mode) ----------------------
+// Physical memory exported as a POSIX file descriptor is reference counted by
+// every importer, so a peer's buffers stay mapped after the peer dies.
+
+namespace {
+struct Vmm {
+  CUresult (*create)(CUmemGenericAllocationHandle *, size_t, const CUmemAllocationProp *, unsigned long long);
+  CUresult (*reserve)(CUdeviceptr *, size_t, size_t, CUdeviceptr, unsigned long long);
+  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+  CUresult (*access)(CUdeviceptr, size_t, const CUmemAccessDesc *, size_t);
+  CUresult (*exportfd)(void *, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long);
+  CUresult (*importfd)(CUmemGenericAllocationHandle *, void *, CUmemAllocationHandleType);
+  CUresult (*granularity)(size_t *, const CUmemAllocationProp *, CUmemAllocationGranularity_flags);
+  CUresult (*release)(CUmemGenericAllocationHandle);
+  bool ok = false;
+};
+
+int vmm(Vmm **out) {
+  static Vmm v;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!v.ok) {
+    struct { const char *name; void **fn; } t[] = {
+        {"cuMemCreate", (void **)&v.create},          {"cuMemAddressReserve", (void **)&v.reserve},
+        {"cuMemMap", (void **)&v.map},                {"cuMemSetAccess", (void **)&v.access},
+        {"cuMemExportToShareableHandle", (void **)&v.exportfd},
+        {"cuMemImportFromShareableHandle", (void **)&v.importfd},
+        {"cuMemGetAllocationGranularity", (void **)&v.granularity},
+        {"cuMemRelease", (void **)&v.release}};
+    for (auto &e : t) {
+      cudaDriverEntryPointQueryResult q;
+      CK(cudaGetDriverEntryPoint(e.name, e.fn, cudaEnableDefault, &q));
+      if (q != cudaDriverEntryPointSuccess || !*e.fn) return set_err(RCV_ECUDA, "%s unavailable", e.name);
+    }
+    v.ok = true;
+  }
+  *out = &v;
+  return RCV_OK;
+}
+
+int vmm_map(Vmm *v, CUmemGenericAllocationHandle h, size_t size, int dev, void **ptr) {
+  CUdeviceptr va = 0;
+  if (v->reserve(&va, size, 0, 0, 0) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuMemAddressReserve");
+  if (v->map(va, size, 0, h, 0) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuMemMap");
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  std::vector<CUmemAccessDesc> acc;
+  for (int d = 0; d < n; ++d) {
+    int can = d == dev;
+    if (!can) cudaDeviceCanAccessPeer(&can, d, dev);
+    if (!can) continue;
+    CUmemAccessDesc a = {};
+    a.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    a.location.id = d;
+    a.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    acc.push_back(a);
+  }
+  if (v->access(va, size, acc.data(), acc.size()) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuMemSetAccess");
+  *ptr = (void *)va;
+  return RCV_OK;
+}
+}  // namespace
+
+int rcv_vmm_alloc(size_t bytes, void **ptr_out, size_t *size_out, int *fd_out) {
+  Vmm *v = nullptr;
+  int rc = vmm(&v);
+  if (rc) return rc;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = dev;
+  prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t gran = 0;
+  if (v->granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS)
+    return set_err(RCV_ECUDA, "cuMemGetAllocationGranularity");
+  const size_t size = (bytes + gran - 1) / gran * gran;
+  CUmemGenericAllocationHandle h;
+  if (v->create(&h, size, &prop, 0) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuMemCreate %zu", size);
+  rc = vmm_map(v, h, size, dev, ptr_out);
+  if (rc) return rc;
+  int fd = -1;
+  if (v->exportfd(&fd, h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) != CUDA_SUCCESS)
+    return set_err(RCV_ECUDA, "cuMemExportToShareableHandle");
+  v->release(h);  // the mapping keeps the physical memory alive
+  *size_out = size;
+  *fd_out = fd;
+  return RCV_OK;
+}
+
+int rcv_vmm_import(int fd, size_t size, int owner_device, void **ptr_out) {
+  Vmm *v = nullptr;
+  int rc = vmm(&v);
+  if (rc) return rc;
+  CUmemGenericAllocationHandle h;
+  if (v->importfd(&h, (void *)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR) != CUDA_SUCCESS)
+    return set_err(RCV_ECUDA, "cuMemImportFromShareableHandle(fd %d)", fd);
+  rc = vmm_map(v, h, size, owner_device, ptr_out);
+  v->release(h);
+  return rc;
+}
+
 int rcv_ipc_import(const void *handle, size_t offset, void **ptr_out) {
   static std::mutex mu;
   static std::vector<std::pair<std::string, void *>> opened;
@@ -1605,6 +1724,11 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       return rc;
     }
     p->comb.max_ctas = env_ctas("RCV_COMB_CTAS", ctx->sms, 0.0);
+    if (d->guarded) {
+      // the combine reads live peers' partials: skip it once one timed out
+      p->comb.guard = (const unsigned int *)ctx->bar.status;
+      p->comb.guard_mask = (unsigned int)(d->live_mask & ~(1ull << ctx->me));
+    }
     p->has_comb = true;
     p->slice_q = d->slice_q;
     p->slice_nr = d->slice_nr;

@@ -93,6 +93,125 @@ class PeerBuffers:
                 for r, (hh, oo) in enumerate(got)]
 
 
+class VmmBuffers:
+    """Shared buffers for real-kill mode: cuMem VMM allocations exported as
+    POSIX file descriptors, passed to every peer over a Unix socket
+    (SCM_RIGHTS) and mapped there.  An importer's mapping holds a reference
+    on the physical memory, so a dead peer's buffers never become invalid
+    addresses for the survivors."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        import os
+        import secrets
+        self.rank, self.world, self.group = rank, world, group
+        tok = [None] * world
+        dist.all_gather_object(tok, secrets.token_hex(8) if rank == 0 else None, group=group)
+        self.job = tok[0]
+        self.dev = torch.cuda.current_device()
+        self._keep = []  # fds and tensors that must outlive the mappings
+        self._os = os
+
+    def share(self, nbytes: int, dtype: torch.dtype):
+        """Allocate nbytes here; returns (local tensor, [ptr of every rank])."""
+        import socket
+        import threading
+        ptr, size, fd = _lib.vmm_alloc(nbytes)
+        addr = "\0rcv-%s-%d-%d" % (self.job, self.rank, len(self._keep))
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(addr)
+        srv.listen(self.world)
+
+        def serve():
+            for _ in range(self.world - 1):
+                conn, _ = srv.accept()
+                socket.send_fds(conn, [b"f"], [fd])
+                conn.close()
+        th = threading.Thread(target=serve, daemon=True)
+        th.start()
+        meta = [None] * self.world
+        dist.all_gather_object(meta, (size, self.dev), group=self.group)
+        ptrs = []
+        for r in range(self.world):
+            if r == self.rank:
+                ptrs.append(ptr)
+                continue
+            c = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            c.connect("\0rcv-%s-%d-%d" % (self.job, r, len(self._keep)))
+            _, fds, _, _ = socket.recv_fds(c, 1, 1)
+            c.close()
+            ptrs.append(_lib.vmm_import(fds[0], meta[r][0], meta[r][1]))
+            self._os.close(fds[0])
+        th.join()
+        srv.close()
+        es = torch.tensor([], dtype=dtype).element_size()
+        local = _lib.tensor_at(ptr, nbytes // es, dtype, torch.device("cuda", self.dev))
+        self._keep.append((fd, local))
+        return local, ptrs
+
+
+class DeadPeerDetector:
+    """Injector for real-kill mode on the survivors: they are not told the
+    schedule.  At a poll point (after_sync, once per iteration, and
+    before_sync of the next) it synchronises the device, reads the barrier
+    status word and reports every replica held by a rank whose barrier wait
+    timed out — the crash-stop detection of comm.py:129-172 driven by the
+    hardware instead of the simulator.  Optionally re-forms the torch
+    process group without the dead ranks (ncclCommShrink via
+    torch.distributed.shrink_group)."""
+
+    def __init__(self, engine: "DistributedGradientCommit", inner=None, shrink: bool = False):
+        self.engine, self.inner, self.shrink = engine, inner, shrink
+        self.known = 0
+        self.detections: List[dict] = []
+
+    def fire(self, phase, bucket=None):
+        out = list(self.inner.fire(phase, bucket)) if self.inner is not None else []
+        if phase not in ("after_sync", "before_sync"):
+            return out
+        import time
+        t0 = time.perf_counter()
+        torch.cuda.synchronize(self.engine.device)
+        bits = int(self.engine.status.item()) & ~self.known
+        if bits:
+            self.known |= bits
+            dead_ranks = [r for r in range(self.engine.world) if (bits >> r) & 1]
+            victims = [rid for rid in self.engine.comm.members if self.engine.rank_of[rid] in dead_ranks]
+            rec = {"phase": phase, "ranks": dead_ranks, "replicas": victims,
+                   "sync_ms": (time.perf_counter() - t0) * 1e3}
+            if self.shrink and hasattr(dist, "shrink_group"):
+                t1 = time.perf_counter()
+                try:
+                    dist.shrink_group(dead_ranks)
+                    rec["shrink_ms"] = (time.perf_counter() - t1) * 1e3
+                except Exception as exc:  # reported, not fatal: NCCL is off the data path
+                    rec["shrink_error"] = repr(exc)[:200]
+            self.detections.append(rec)
+            out += victims
+        return out
+
+
+class RealKill:
+    """Victim-side injector: at (step, phase, bucket) this process drains its
+    own GPU work and dies by SIGKILL (the paper's failure simulator,
+    PAPER.md:715-726).  The drain makes sure no survivor is mid-read of
+    this rank's partials when the process disappears."""
+
+    def __init__(self, step: int, phase: str, bucket=None, drain_s: float = 0.3):
+        self.at = (step, phase, bucket)
+        self.step = -1
+        self.drain_s = drain_s
+
+    def fire(self, phase, bucket=None):
+        if (self.step, phase, bucket if phase == "during_sync" else None) == self.at:
+            import os
+            import signal
+            import time
+            torch.cuda.synchronize()
+            time.sleep(self.drain_s)
+            os.kill(os.getpid(), signal.SIGKILL)
+        return []
+
+
 class DistributedGradientCommit(GradientCommit):
     """``GradientCommit`` with replicas spread over the ranks of a process
     group, (w_init + spares) / world consecutive replicas per rank."""
@@ -103,7 +222,8 @@ class DistributedGradientCommit(GradientCommit):
                  policy_kind: str = "static", spares: int = 0,
                  variant: int = _lib.VARIANT_AUTO,
                  combine_variant: int = _lib.VARIANT_AUTO,
-                 pool_slots: int = 8, barrier_timeout_s: float = 30.0):
+                 pool_slots: int = 8, barrier_timeout_s: float = 30.0,
+                 real_kill: bool = False):
         if policy_kind not in ("static", "adaptive"):
             raise ValueError("unknown policy kind %r" % (policy_kind,))
         self.rank = dist.get_rank(group) if rank is None else rank
@@ -131,20 +251,31 @@ class DistributedGradientCommit(GradientCommit):
         self._es = torch.tensor([], dtype=dtype).element_size()
 
         local = [r for r in members if self.rank_of[r] == self.rank]
-        store = torch.zeros(per * numel, dtype=dtype, device=self.device)
-        self.grads = {r: store[i * numel:(i + 1) * numel] for i, r in enumerate(local)}
         self.lmax = max(hi - lo for lo, hi in self.bounds)
         self.pool_slots = pool_slots
-        self.pool = torch.empty(3 * pool_slots * self.lmax, dtype=dtype, device=self.device)
-        self.flags = torch.zeros(64, dtype=torch.int64, device=self.device)
+        self.real_kill = real_kill
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.timeout_ns = int(barrier_timeout_s * 1e9)
-        pb = PeerBuffers(self.rank, self.world, group)
-        store_ptr = pb.share(store)
+        if real_kill:
+            # VMM memory: survivors' mappings outlive a dead exporter
+            vb = VmmBuffers(self.rank, self.world, group)
+            self._shared = vb
+            store, store_ptr = vb.share(per * numel * self._es, dtype)
+            self.pool, self.pool_ptr = vb.share(3 * pool_slots * self.lmax * self._es, dtype)
+            self.flags, self.flag_ptr = vb.share(64 * 8, torch.int64)
+            store.zero_()
+            self.flags.zero_()
+        else:
+            store = torch.zeros(per * numel, dtype=dtype, device=self.device)
+            self.pool = torch.empty(3 * pool_slots * self.lmax, dtype=dtype, device=self.device)
+            self.flags = torch.zeros(64, dtype=torch.int64, device=self.device)
+            pb = PeerBuffers(self.rank, self.world, group)
+            store_ptr = pb.share(store)
+            self.pool_ptr = pb.share(self.pool)
+            self.flag_ptr = pb.share(self.flags)
+        self.grads = {r: store[i * numel:(i + 1) * numel] for i, r in enumerate(local)}
         self.grad_ptr = {r: store_ptr[self.rank_of[r]] + (r % per) * numel * self._es
                          for r in members}
-        self.pool_ptr = pb.share(self.pool)
-        self.flag_ptr = pb.share(self.flags)
         self.rt = _lib.BucketRuntime(self.world, self.rank, self.flags, self.flag_ptr,
                                      self.status, self.timeout_ns)
         self._plan_key = None
@@ -237,7 +368,8 @@ class DistributedGradientCommit(GradientCommit):
             variant=self.variant, comb_variant=self.combine_variant,
             live_mask=mask, participate=int(part),
             remote_in=sum(1 for rk, _ in slot_of.values() if rk != self.rank),
-            remote_out=sum(1 for r in prim if not self._holds(r)))
+            remote_out=sum(1 for r in prim if not self._holds(r)),
+            guarded=int(self.real_kill))
         self.rt.set_plan(d, keep)
 
     def _reduce_bucket(self, k: int, leaves) -> int:
