@@ -8,6 +8,20 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 def log(*a):
     print("[rank %s %.2f]" % (os.environ.get("RANK"), time.time() % 1000), *a, file=sys.stderr, flush=True)
 
+if len(sys.argv) > 1 and sys.argv[1] == "--spawn":
+    # plain launcher: torchrun's agent would SIGTERM the survivors
+    import subprocess
+    n = int(sys.argv[2])
+    ps = [subprocess.Popen([sys.executable, __file__], env=dict(os.environ, RANK=str(r), LOCAL_RANK=str(r),
+          WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT="29544")) for r in range(n)]
+    for p in ps:
+        try:
+            p.wait(timeout=90)
+        except subprocess.TimeoutExpired:
+            print("rank pid", p.pid, "hung; killing", file=sys.stderr, flush=True)
+            p.kill()
+    print("exit codes", [p.returncode for p in ps], file=sys.stderr, flush=True)
+    sys.exit(0)
 local = int(os.environ["LOCAL_RANK"]); world = int(os.environ["WORLD_SIZE"]); rank = int(os.environ["RANK"])
 torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
