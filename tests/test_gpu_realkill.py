@@ -34,7 +34,7 @@ def _worker(rank, world, port, q):
         dev = [torch.from_numpy(h).cuda() for h in host]
         want = fold.canonical_tree(dict(enumerate(host)), b) / np.float32(b)
         eng = DistributedGradientCommit(numel, w, g, 4, real_kill=True, barrier_timeout_s=1.0)
-        inj = RealKill(1, "during_sync", 2) if rank == 1 else DeadPeerDetector(eng, shrink=True)
+        inj = RealKill(1, "during_sync", 2) if rank == 1 else DeadPeerDetector(eng, shrink=False)
         res = []
         for t in range(4):
             inj.step = t
@@ -47,7 +47,10 @@ def _worker(rank, world, port, q):
     except Exception:
         import traceback
         q.put((rank, traceback.format_exc(), None))
-    # survivors leave without tearing the (now broken) NCCL group down
+    # flush the result (Queue.put is asynchronous), then leave without
+    # tearing the now-broken NCCL group down
+    q.close()
+    q.join_thread()
     os._exit(0)
 
 
