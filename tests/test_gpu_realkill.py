@@ -34,7 +34,7 @@ def _worker(rank, world, port, q):
         dev = [torch.from_numpy(h).cuda() for h in host]
         want = fold.canonical_tree(dict(enumerate(host)), b) / np.float32(b)
         eng = DistributedGradientCommit(numel, w, g, 4, real_kill=True, barrier_timeout_s=1.0)
-        inj = RealKill(1, "during_sync", 2) if rank == 1 else DeadPeerDetector(eng, shrink=False)
+        inj = RealKill(1, "during_sync", 2) if rank == 1 else DeadPeerDetector(eng, shrink=True)
         res = []
         for t in range(4):
             inj.step = t
