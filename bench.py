@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--numel", type=int, default=D_GPT2)
+    ap.add_argument("--buckets", type=int, default=K)
     ap.add_argument("--no-fail", action="store_true")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--combine-variant", type=int, default=0)
@@ -129,12 +130,13 @@ class Clocks:
 class StepKill:
     """Kill VICTIM during_sync on VICTIM_BUCKET at one step (configs[1])."""
 
-    def __init__(self, at_step):
+    def __init__(self, at_step, bucket=VICTIM_BUCKET):
         self.at_step = at_step
+        self.bucket = bucket
         self.step = -1
 
     def fire(self, phase, bucket=None):
-        if self.step == self.at_step and phase == "during_sync" and bucket == VICTIM_BUCKET:
+        if self.step == self.at_step and phase == "during_sync" and bucket == self.bucket:
             return [VICTIM]
         return []
 
@@ -281,12 +283,12 @@ def run_ours(args):
     fail_step = -1 if args.no_fail else args.warmup + args.steps // 2
     if world > 1:
         from paper_2605_11215_b200.dist import DistributedGradientCommit
-        eng = DistributedGradientCommit(numel, W, G, K, variant=args.variant,
+        eng = DistributedGradientCommit(numel, W, G, args.buckets, variant=args.variant,
                                         combine_variant=args.combine_variant)
     else:
-        eng = GradientCommit(numel, W, G, K, placement={r: dev for r in range(W)},
+        eng = GradientCommit(numel, W, G, args.buckets, placement={r: dev for r in range(W)},
                              variant=args.variant)
-    kill = StepKill(fail_step)
+    kill = StepKill(fail_step, min(VICTIM_BUCKET, args.buckets - 1))
 
     def leaf(m, rid):
         return leaves[m]
@@ -397,9 +399,9 @@ def run_ours(args):
         "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": "gpt2-124m gradient commit, DP=8, M=32, K=20, "
-                               "replica 3 killed during_sync:7",
-                   "numel": numel, "replicas": W, "microbatches": M, "buckets": K,
+        "config": {"workload": "gpt2-124m gradient commit, DP=8, M=32, K=%d, "
+                               "replica 3 killed during_sync:%d" % (args.buckets, kill.bucket),
+                   "numel": numel, "replicas": W, "microbatches": M, "buckets": args.buckets,
                    "tokens_per_microbatch": TOKENS_PER_MB,
                    "fail_step": fail_step, "placement": "8 replicas on 1 GPU" if world == 1
                    else "%d replicas per rank, NVLink P2P" % (W // world), "l2": "inputs 15.9 GB >> 126 MB L2",
