@@ -58,6 +58,27 @@ def main():
             res.append({"pattern": name, "variant": vname, "ms": ms,
                         "gbs_per_direction": n * 4 / ms / 1e6,
                         "note": "every rank moves 256 MB at once (both directions loaded)"})
+    # the combine's shapes: fold one slice from every rank (peers over NVLink)
+    # into a local output; store one local slice into every rank; both at once
+    peers = [r for r in range(world) if r != rank]
+    sl = n // world
+    for vname, v in (("tma", _lib.VARIANT_TMA), ("direct", _lib.VARIANT_DIRECT)):
+        blocks = [(src_p[r] + rank * sl * 4, r, 0, _lib.F32) for r in range(world)]
+        width = 1 << max(0, (world - 1).bit_length())
+        pull = _lib.TreePlan(blocks, width, [dst.data_ptr() + rank * sl * 4], _lib.F32, 0.0, v)
+        ms = timeit(lambda: pull.run(0, 0, sl, stream))
+        res.append({"pattern": "allgather-pull-fold", "variant": vname, "ms": ms,
+                    "nvlink_in_gbs": len(peers) * sl * 4 / ms / 1e6})
+        push = _lib.TreePlan([(src.data_ptr() + rank * sl * 4, 0, 0, _lib.F32)], 1,
+                             [dst_p[r] + rank * sl * 4 for r in range(world)], _lib.F32, 0.0, v)
+        ms = timeit(lambda: push.run(0, 0, sl, stream))
+        res.append({"pattern": "push-to-all", "variant": vname, "ms": ms,
+                    "nvlink_out_gbs": len(peers) * sl * 4 / ms / 1e6})
+        both = _lib.TreePlan(blocks, width, [dst_p[r] + rank * sl * 4 for r in range(world)],
+                             _lib.F32, 0.0, v)
+        ms = timeit(lambda: both.run(0, 0, sl, stream))
+        res.append({"pattern": "combine(pull-all+push-all)", "variant": vname, "ms": ms,
+                    "nvlink_gbs_per_direction": len(peers) * sl * 4 / ms / 1e6})
     # copy engine
     ms = timeit(lambda: torch.cuda.current_stream().synchronize() if False else
                 _lib.load().rcv_copy(dst_p[peer], src.data_ptr(), n * 4, stream))
