@@ -370,11 +370,14 @@ def run_ours(args):
     per_kind = {}
     for kind, k in kinds.items():
         sec = k["ms"] / 1e3
+        # NVLink per direction: this rank's remote reads arrive inbound while
+        # the peers' reads of its slices leave outbound (and its remote
+        # stores leave while the peers' arrive), so with symmetric traffic
+        # each direction carries remote reads + remote writes
         per_kind[kind] = {
             "launches": k["launches"], "mean_launch_us": 1e3 * k["ms"] / k["launches"],
             "hbm_gbs": k["bytes"] / sec / 1e9 if sec else None,
-            "nvlink_in_gbs": k["nvl_in"] / sec / 1e9 if sec else None,
-            "nvlink_out_gbs": k["nvl_out"] / sec / 1e9 if sec else None}
+            "nvlink_gbs_per_direction": (k["nvl_in"] + k["nvl_out"]) / sec / 1e9 if sec else None}
     dom = max(kinds, key=lambda kk: kinds[kk]["ms"]) if kinds else None
     fail_idx = [i for i, o in enumerate(outcomes) if o.events]
     normal = [ms for i, ms in enumerate(step_ms) if i not in fail_idx]
@@ -441,8 +444,8 @@ def roofline(dom, per_kind, peak, peak_kind):
     if dom is None:
         return None
     k = per_kind[dom]
-    if dom == "combine" and (k["nvlink_in_gbs"] or 0) > 0:
-        ach = max(k["nvlink_in_gbs"], k["nvlink_out_gbs"])
+    if dom == "combine" and (k["nvlink_gbs_per_direction"] or 0) > 0:
+        ach = k["nvlink_gbs_per_direction"]
         return {"bound": "nvlink", "achieved": ach, "peak": NVLINK_PEAK, "unit": "GB/s",
                 "frac": ach / NVLINK_PEAK, "traffic": None, "peak_kind": "measured peer copy",
                 "kernel": "fold_tma_kernel combine (rcv_tree_commit over peer pointers)",

@@ -14,6 +14,6 @@ for cfg in "$@"; do
 import json,sys
 d=json.loads([l for l in open('$OUT/sweep_$i.json') if l.startswith('{')][-1])
 k=d['kernels']
-print('cfg=[$cfg] ms/step %.3f' % d['ms_per_step'], ' '.join('%s:%.0fus' % (n, v['mean_launch_us']) for n, v in k.items()), 'comb nvl in/out %.0f/%.0f' % (k['combine']['nvlink_in_gbs'], k['combine']['nvlink_out_gbs']))
+print('cfg=[$cfg] ms/step %.3f' % d['ms_per_step'], ' '.join('%s:%.0fus' % (n, v['mean_launch_us']) for n, v in k.items()), 'comb nvl/dir %.0f' % k['combine']['nvlink_gbs_per_direction'])
 " || echo "cfg=[$cfg] failed"
 done

@@ -200,6 +200,11 @@ struct FoldParams {
   // real-kill mode: skip the whole launch when a live peer has timed out
   const unsigned int *guard;  // device status word (NULL: unguarded)
   unsigned int guard_mask;    // the peers this launch reads
+  // forest (ProgForest): root f is a perfect tree of height root_L[f] over
+  // inputs [root_first[f], root_first[f] + 2^root_L[f]), stored to out[f]
+  int n_roots;
+  uint8_t root_L[8];
+  uint8_t root_first[8];
   // canonical tree (ProgTree): heap-indexed nodes, id = 2^(L-level)-1+idx
   int8_t node_in[2 * RCV_MAX_IN - 1];    // input feeding the node, or -1
   uint8_t present[2 * RCV_MAX_IN - 1];   // subtree holds at least one input
@@ -287,6 +292,49 @@ template <int L> struct ProgFull {
   }
 };
 
+// Several disjoint perfect subtrees in one pass (a rank's local cover after
+// a failure, e.g. 8 + 4 + 2 + 1 leaves): each root is stored to its own
+// output, without the divisor (pre-reduce partials).
+struct ProgForest {
+  static constexpr bool kMulti = true;
+  template <typename V, typename Ld, typename St>
+  __device__ __forceinline__ static void run(const FoldParams &p, const Ld &ld, const St &st) {
+    for (int f = 0; f < p.n_roots; ++f) {
+      const int base = p.root_first[f];
+      auto sub = [&](int i) { return ld(base + i); };
+      V r;
+      switch (p.root_L[f]) {
+        case 0: r = ProgFull<0>::template node<0, 0, V>(sub); break;
+        case 1: r = ProgFull<1>::template node<1, 0, V>(sub); break;
+        case 2: r = ProgFull<2>::template node<2, 0, V>(sub); break;
+        case 3: r = ProgFull<3>::template node<3, 0, V>(sub); break;
+        case 4: r = ProgFull<4>::template node<4, 0, V>(sub); break;
+        case 5: r = ProgFull<5>::template node<5, 0, V>(sub); break;
+        default: r = ProgFull<6>::template node<6, 0, V>(sub); break;
+      }
+      st(f, r);
+    }
+  }
+};
+
+template <typename Prog, typename = void> struct IsMulti { static constexpr bool value = false; };
+template <typename Prog> struct IsMulti<Prog, decltype(void(Prog::kMulti))> {
+  static constexpr bool value = Prog::kMulti;
+};
+
+// Evaluate and store one vector position: single-result programs write the
+// (scaled) result to every output, multi-root programs one root per output.
+template <typename Prog, typename V, typename Ld>
+__device__ __forceinline__ void emit(const FoldParams &p, const Ld &ld, unsigned long long off) {
+  if constexpr (IsMulti<Prog>::value) {
+    Prog::template run<V>(p, ld, [&](int j, V r) { st_vec(p.out[j] + off, r); });
+  } else {
+    V r = Prog::template eval<V>(p, ld);
+    if (p.divisor != 0.0) r = vdiv(r, p.divisor);
+    for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + off, r);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // DIRECT variant: 128-bit LDG straight from (local or peer) global memory
 
@@ -301,9 +349,7 @@ __global__ void __launch_bounds__(256)
       const bool b = p.bf16[i];
       return ld_vec<A>(p.in[i] + v * (b ? 8ull : 16ull), b);
     };
-    V r = Prog::template eval<V>(p, ld);
-    if (p.divisor != 0.0) r = vdiv(r, p.divisor);
-    for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + v * 16ull, r);
+    emit<Prog, V>(p, ld, v * 16ull);
   }
 }
 
@@ -415,10 +461,7 @@ __global__ void __launch_bounds__(TMA_THREADS)
         const bool b = p.bf16[i];
         return lds_vec<A>(stage + p.smem_off[i] + (size_t)vi * (b ? 8 : 16), b);
       };
-      V r = Prog::template eval<V>(p, ld);
-      if (p.divisor != 0.0) r = vdiv(r, p.divisor);
-      const unsigned long long off = (v0 + vi) * 16ull;
-      for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + off, r);
+      emit<Prog, V>(p, ld, (v0 + vi) * 16ull);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -676,6 +719,9 @@ struct FoldReq {
   unsigned int guard_mask = 0;
   int tree_L = -1;  // >= 0: canonical tree tables below are valid
   int full_L = -1;  // >= 0: inputs are the 2^full_L leaves of a perfect tree
+  int n_roots = 0;  // > 0: a forest of perfect trees, one output per root
+  uint8_t root_L[8] = {};
+  uint8_t root_first[8] = {};
   int8_t node_in[2 * RCV_MAX_IN - 1];
   uint8_t present[2 * RCV_MAX_IN - 1];
 };
@@ -755,6 +801,9 @@ void fill_vec_params(FoldParams &p, const FoldReq &r, unsigned long long e0,
   p.divisor = r.divisor;
   p.guard = r.guard;
   p.guard_mask = r.guard_mask;
+  p.n_roots = r.n_roots;
+  memcpy(p.root_L, r.root_L, sizeof p.root_L);
+  memcpy(p.root_first, r.root_first, sizeof p.root_first);
   if (r.tree_L >= 0) {
     const int nodes = (2 << r.tree_L) - 1;
     memcpy(p.node_in, r.node_in, nodes);
@@ -851,6 +900,7 @@ int launch_vec(const FoldReq &r, bool tma, const TmaGeom &g, int maxd,
                unsigned long long e0, unsigned long long nvec, cudaStream_t st, int sms) {
 #define RCV_LAUNCH(PROG) \
   return tma ? launch_tma_p<A, PROG>(r, g, e0, nvec, st, sms) : launch_direct_p<A, PROG>(r, e0, nvec, st, sms)
+  if (r.n_roots > 0) RCV_LAUNCH(ProgForest);
   if (r.full_L >= 0 && r.full_L <= 6) {
     switch (r.full_L) {
       case 0: RCV_LAUNCH(ProgFull<0>);
@@ -906,6 +956,8 @@ int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int s
   const bool f64 = r.acc_dt == RCV_F64;
   const int E = f64 ? 2 : 4;
   int h = variant == RCV_VARIANT_SCALAR ? -1 : common_head(r);
+  if (r.n_roots > 0 && (h != 0 || (numel % (2 * E)) != 0))
+    return set_err(RCV_EINVAL, "forest fold needs 16-byte aligned, vector-multiple ranges");
   if (h < 0 || (size_t)h >= numel) {
     return f64 ? launch_scalar<double>(r, maxd, 0, numel, st, sms)
                : launch_scalar<float>(r, maxd, 0, numel, st, sms);
@@ -1547,6 +1599,9 @@ struct rcv_plan {
   rcv_ctx *ctx = nullptr;
   std::vector<FoldReq> pre;
   std::vector<int> pre_count;
+  bool has_forest = false;  // all pre nodes fused into one launch
+  FoldReq forest;
+  int forest_count = 0;
   size_t set_stride = 0;
   bool has_comb = false;
   FoldReq comb;
@@ -1716,6 +1771,46 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
     p->pre_count.push_back(d->pre_counts[i]);
     off += d->pre_counts[i];
   }
+  // several full pre-reduce nodes (each 2^level leaves, all present) fuse
+  // into one forest launch; plain nodes stay separate requests
+  if (d->n_pre > 1 && d->n_pre <= 8 && getenv("RCV_NO_FOREST") == nullptr) {
+    bool ok = true;
+    int total = 0;
+    for (int i = 0; i < d->n_pre && ok; ++i) {
+      ok = d->pre_counts[i] == (int)d->pre_leaves[i];
+      total += d->pre_counts[i];
+    }
+    ok = ok && total <= RCV_MAX_IN;
+    if (ok) {
+      FoldReq &r = p->forest;
+      int k = 0;
+      for (int i = 0; i < d->n_pre; ++i) {
+        int L = 0;
+        while ((1 << L) < d->pre_counts[i]) ++L;
+        r.root_L[i] = (uint8_t)L;
+        r.root_first[i] = (uint8_t)k;
+        for (int j = 0; j < d->pre_counts[i]; ++j, ++k) {
+          const rcv_block &b = d->pre_blocks[k];
+          int rc = check_dtype(d->acc_dtype, b.dtype);
+          if (rc) {
+            delete p;
+            return rc;
+          }
+          r.in[k] = (const char *)b.ptr;
+          r.in_dt[k] = b.dtype;
+          r.op[k] = 0;  // unused by the forest evaluator
+        }
+        r.out[i] = (char *)d->pre_out[i];
+      }
+      r.n_in = k;
+      r.n_out = d->n_pre;
+      r.n_roots = d->n_pre;
+      r.acc_dt = d->acc_dtype;
+      r.max_ctas = env_ctas("RCV_PRE_CTAS", ctx->sms, 0.0);
+      p->has_forest = true;
+      p->forest_count = k;
+    }
+  }
   if (d->n_comb > 0 && d->participate) {
     int rc = prepare_tree(d->comb_blocks, d->n_comb, d->n_leaves, d->n_comb_out, d->comb_out,
                           d->acc_dtype, d->divisor, p->comb);
@@ -1779,7 +1874,16 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
       if (rc) return rc;
     }
   }
-  for (size_t i = 0; i < p->pre.size(); ++i) {
+  bool forest_done = false;
+  if (p->has_forest && n % 64 == 0) {
+    FoldReq r = p->forest;
+    shift(r, lo, set_off);
+    const double bytes = (double)(p->forest_count + r.n_out) * n * esize(r.acc_dt);
+    int rc = timed(c, c->side, 0, bytes, 0, 0,
+                   [&]() { return run_fold(r, n, p->variant, c->side, c->sms); });
+    forest_done = rc == RCV_OK;  // misaligned leaves: fall back to per-node launches
+  }
+  for (size_t i = 0; i < p->pre.size() && !forest_done; ++i) {
     FoldReq r = p->pre[i];
     shift(r, lo, set_off);
     const double bytes = (double)(p->pre_count[i] + 1) * n * esize(r.acc_dt);
