@@ -391,8 +391,8 @@ def run_ours(args):
     # e2e through the public API with host buffers: pinned host gradients
     # copied in every step, committed gradient copied out every step
     e2e = None
-    if args.e2e_steps > 0 and world == 1:
-        e2e = e2e_leg(args, dev, leaves, numel)
+    if args.e2e_steps > 0:
+        e2e = e2e_leg(args, dev, leaves, numel, world)
     if world > 1:
         eng.check_peers()
 
@@ -457,33 +457,43 @@ def roofline(dom, per_kind, peak, peak_kind):
             "mean_launch_us": k["mean_launch_us"], "launches_timed": k["launches"]}
 
 
-def e2e_leg(args, dev, leaves, numel):
-    """Same step through GradientCommit with HOST inputs: every step copies
-    the 32 microbatch gradients host->device (pinned) and the committed
-    gradient device->host, inside the timed region."""
+def e2e_leg(args, dev, leaves, numel, world=1):
+    """The same step through the public API with HOST inputs: every step each
+    rank copies its replicas' microbatch gradients host->device (pinned) and
+    its committed gradient device->host, inside the timed region (max over
+    ranks).  Failure-free steps: the host copies are the subject here."""
     import torch
     from paper_2605_11215_b200.commit import GradientCommit
+    if world > 1:
+        from paper_2605_11215_b200.dist import DistributedGradientCommit
+        eng = DistributedGradientCommit(numel, W, G, args.buckets, variant=args.variant,
+                                        combine_variant=args.combine_variant)
+    else:
+        eng = GradientCommit(numel, W, G, args.buckets, placement={r: dev for r in range(W)},
+                             variant=args.variant)
+    mine = [r for r in range(W) if r in eng.grads]
+    idx = [m for r in mine for m in range(r * G, (r + 1) * G)]  # failure-free canonical ranges
     try:
-        host = [torch.empty(numel, dtype=torch.float32, pin_memory=True) for _ in range(M)]
+        host = {m: torch.empty(numel, dtype=torch.float32, pin_memory=True) for m in idx}
         pinned = True
     except RuntimeError:
-        host = [torch.empty(numel, dtype=torch.float32) for _ in range(M)]
+        host = {m: torch.empty(numel, dtype=torch.float32) for m in idx}
         pinned = False
-    for h, l in zip(host, leaves):
-        h.copy_(l)
+    for m in idx:
+        host[m].copy_(leaves[m])
     out_host = torch.empty(numel, dtype=torch.float32, pin_memory=pinned)
-    eng = GradientCommit(numel, W, G, K, placement={r: dev for r in range(W)})
-    dev_slots = leaves  # reuse the HBM slots as H2D targets
     stream = torch.cuda.current_stream(dev)
 
     def one(s):
-        for h, d in zip(host, dev_slots):
-            d.copy_(h, non_blocking=True)
-        eng.step(s, lambda m, rid: dev_slots[m])
-        out_host.copy_(eng.grads[eng.comm.members[0]], non_blocking=True)
+        for m in idx:
+            leaves[m].copy_(host[m], non_blocking=True)
+        eng.step(s, lambda m, rid: leaves[m])
+        out_host.copy_(eng.grads[mine[0]], non_blocking=True)
 
     one(0)
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     a = torch.cuda.Event(enable_timing=True)
     z = torch.cuda.Event(enable_timing=True)
     a.record(stream)
@@ -492,12 +502,16 @@ def e2e_leg(args, dev, leaves, numel):
     z.record(stream)
     torch.cuda.synchronize()
     ms = a.elapsed_time(z) / args.e2e_steps
-    bi = M * numel * 4
-    bo = numel * 4
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    bi = M * numel * 4          # every microbatch gradient, summed over ranks
+    bo = world * numel * 4      # one committed gradient per rank
     return {"value": M * TOKENS_PER_MB / (ms / 1e3), "unit": "tokens/s",
             "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "ms_per_step": ms,
             "steps": args.e2e_steps, "pinned": pinned,
-            "h2d_gbs": (bi + bo) / (ms / 1e3) / 1e9}
+            "pcie_gbs_per_gpu": (bi + bo) / world / (ms / 1e3) / 1e9}
 
 
 def main():

@@ -1853,6 +1853,9 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
   if (n == 0) return RCV_OK;
   rcv_ctx *c = p->ctx;
   cudaStream_t main = (cudaStream_t)main_stream;
+  // while timing launch by launch everything runs on the caller's stream, so
+  // each kernel's duration is its own (no cross-stream overlap stretching it)
+  cudaStream_t side = c->timing ? main : c->side;
   const int es = esize(p->has_comb ? p->comb.acc_dt : RCV_F32);
   if (!c->in_step) {
     c->in_step = true;  // leaves were produced on the caller's stream
@@ -1868,9 +1871,9 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
   const unsigned long long j = c->calls++;
   const size_t set_off = (j % 3) * p->set_stride;
   if (j >= 2) {
-    CK(cudaStreamWaitEvent(c->side, c->ev_arrived[(j - 2) % 3], 0));
+    CK(cudaStreamWaitEvent(side, c->ev_arrived[(j - 2) % 3], 0));
     if (j >= 3) {
-      int rc = ctx_flush(c, c->side, (long long)j - 3);
+      int rc = ctx_flush(c, side, (long long)j - 3);
       if (rc) return rc;
     }
   }
@@ -1879,19 +1882,19 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
     FoldReq r = p->forest;
     shift(r, lo, set_off);
     const double bytes = (double)(p->forest_count + r.n_out) * n * esize(r.acc_dt);
-    int rc = timed(c, c->side, 0, bytes, 0, 0,
-                   [&]() { return run_fold(r, n, p->variant, c->side, c->sms); });
+    int rc = timed(c, side, 0, bytes, 0, 0,
+                   [&]() { return run_fold(r, n, p->variant, side, c->sms); });
     forest_done = rc == RCV_OK;  // misaligned leaves: fall back to per-node launches
   }
   for (size_t i = 0; i < p->pre.size() && !forest_done; ++i) {
     FoldReq r = p->pre[i];
     shift(r, lo, set_off);
     const double bytes = (double)(p->pre_count[i] + 1) * n * esize(r.acc_dt);
-    int rc = timed(c, c->side, 0, bytes, 0, 0,
-                   [&]() { return run_fold(r, n, p->variant, c->side, c->sms); });
+    int rc = timed(c, side, 0, bytes, 0, 0,
+                   [&]() { return run_fold(r, n, p->variant, side, c->sms); });
     if (rc) return rc;
   }
-  CK(cudaEventRecord(c->ev_ready, c->side));
+  CK(cudaEventRecord(c->ev_ready, side));
   CK(cudaStreamWaitEvent(main, c->ev_ready, 0));
   int rc = ctx_barrier(c, p->live_mask, p->participate, main);
   if (rc) return rc;
