@@ -159,16 +159,6 @@ __device__ __forceinline__ typename VecT<A>::V lds_vec(const unsigned char *p,
 template <typename V> __device__ __forceinline__ void st_vec(char *p, const V &v) {
   *reinterpret_cast<V *>(p) = v;
 }
-// streaming store (st.global.cs): the committed gradient is not re-read by
-// this kernel, so it should not displace inputs in L2
-__device__ __forceinline__ void st_vec_cs(char *p, const float4 &v) {
-  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
-               "f"(v.w)
-               : "memory");
-}
-__device__ __forceinline__ void st_vec_cs(char *p, const double2 &v) {
-  asm volatile("st.global.cs.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
-}
 
 // Fixed-capacity register stack.  Indices are compared against the (warp-
 // uniform) stack pointer with fully unrolled predicates, so the array stays in
@@ -215,8 +205,6 @@ struct FoldParams {
   int n_roots;
   uint8_t root_L[8];
   uint8_t root_first[8];
-  int store_cs;   // outputs with st.global.cs
-  int load_hint;  // TMA loads with an L2 evict_first policy
   // canonical tree (ProgTree): heap-indexed nodes, id = 2^(L-level)-1+idx
   int8_t node_in[2 * RCV_MAX_IN - 1];    // input feeding the node, or -1
   uint8_t present[2 * RCV_MAX_IN - 1];   // subtree holds at least one input
@@ -343,10 +331,7 @@ __device__ __forceinline__ void emit(const FoldParams &p, const Ld &ld, unsigned
   } else {
     V r = Prog::template eval<V>(p, ld);
     if (p.divisor != 0.0) r = vdiv(r, p.divisor);
-    if (p.store_cs)
-      for (int j = 0; j < p.n_out; ++j) st_vec_cs(p.out[j] + off, r);
-    else
-      for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + off, r);
+    for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + off, r);
   }
 }
 
@@ -412,14 +397,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src,
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes,
-                                              uint64_t *bar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
-      : "memory");
-}
 
 template <typename A, typename Prog>
 __global__ void __launch_bounds__(TMA_THREADS)
@@ -448,9 +425,7 @@ __global__ void __launch_bounds__(TMA_THREADS)
     if (lane == 0) {
       int s = 0;
       uint32_t phase = 0;
-      uint64_t policy = 0;
-      if (p.load_hint)  // every input byte is read exactly once
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+
       for (unsigned long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
         mbar_wait(&empty[s], phase ^ 1);
         const unsigned long long v0 = t * tv;
@@ -461,10 +436,7 @@ __global__ void __launch_bounds__(TMA_THREADS)
         unsigned char *stage = smem + (size_t)s * p.stage_bytes;
         for (int i = 0; i < p.n_in; ++i) {
           const uint32_t vb = p.bf16[i] ? 8u : 16u;
-          if (p.load_hint)
-            bulk_g2s_hint(stage + p.smem_off[i], p.in[i] + v0 * vb, nv * vb, &full[s], policy);
-          else
-            bulk_g2s(stage + p.smem_off[i], p.in[i] + v0 * vb, nv * vb, &full[s]);
+          bulk_g2s(stage + p.smem_off[i], p.in[i] + v0 * vb, nv * vb, &full[s]);
         }
         if (++s == p.stages) {
           s = 0;
@@ -831,10 +803,6 @@ void fill_vec_params(FoldParams &p, const FoldReq &r, unsigned long long e0,
   p.guard = r.guard;
   p.guard_mask = r.guard_mask;
   p.n_roots = r.n_roots;
-  static const int cs = getenv("RCV_STORE_CS") ? atoi(getenv("RCV_STORE_CS")) : 0;
-  static const int hint = getenv("RCV_LOAD_HINT") ? atoi(getenv("RCV_LOAD_HINT")) : 0;
-  p.store_cs = cs;
-  p.load_hint = hint;
   memcpy(p.root_L, r.root_L, sizeof p.root_L);
   memcpy(p.root_first, r.root_first, sizeof p.root_first);
   if (r.tree_L >= 0) {
