@@ -972,6 +972,12 @@ int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int s
   }
   if (nvec) {
     TmaGeom g;
+    // AUTO, from measurement (profiles/r1/variant_ab.txt): the straight-line
+    // perfect-tree and forest evaluators run fastest from registers with
+    // LDG.128 (93% of HBM at N=1 vs 87% through the TMA ring); evaluators
+    // with warp-uniform branches (ProgTree, ProgStack, ProgLeft) keep the TMA
+    // ring, which decouples their loads from the control flow.
+    if (variant == RCV_VARIANT_AUTO && (r.full_L >= 0 || r.n_roots > 0)) variant = RCV_VARIANT_DIRECT;
     bool use_tma = variant == RCV_VARIANT_TMA || variant == RCV_VARIANT_AUTO;
     if (use_tma && !tma_geom(r, &g)) {
       if (variant == RCV_VARIANT_TMA)
