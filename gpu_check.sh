@@ -15,7 +15,7 @@ if [ "$NCU" = "1" ] && [ $RC = 0 ]; then
   timeout 300 $SMALL > $OUT/ncu_plain_$TAG.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file $OUT/launches_$TAG.csv $SMALL > $OUT/ncu_launch_$TAG.log 2>&1; echo "ncu launches rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${NCU_K:-fold_tma} \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${NCU_K:-fold_} \
       -s ${NCU_S:-40} -c 1 -o $OUT/prof_$TAG $SMALL > $OUT/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
   tail -2 $OUT/ncu_full_$TAG.log
 fi
