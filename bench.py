@@ -437,7 +437,9 @@ def run_ours(args):
 
 
 NVLINK_PEAK = 770.0  # GB/s per direction, measured peer copy (B200_PROFILING.md)
-TRAFFIC = {"fused": 977.8e6}  # dram read+write bytes per launch, ncu --set full (profiles/r1)
+# dram read+write bytes per launch of the dominant kernel, ncu --set full
+# (profiles/r1/ncu_full_fold_direct_ProgFull5.txt: 796.4 MB + 147.9 MB)
+TRAFFIC = {"fused": 944.3e6}
 
 
 def roofline(dom, per_kind, peak, peak_kind):
@@ -453,7 +455,7 @@ def roofline(dom, per_kind, peak, peak_kind):
     return {"bound": "hbm", "achieved": k["hbm_gbs"], "peak": peak, "unit": "GB/s",
             "frac": k["hbm_gbs"] / peak if k["hbm_gbs"] else None,
             "traffic": TRAFFIC.get(dom), "peak_kind": peak_kind,
-            "kernel": "fold_tma_kernel<float, ProgFull<5>> (rcv_tree_commit, %s)" % dom,
+            "kernel": "fold_direct_kernel<float, ProgFull<L>> (rcv_tree_commit AUTO, %s)" % dom,
             "mean_launch_us": k["mean_launch_us"], "launches_timed": k["launches"]}
 
 
