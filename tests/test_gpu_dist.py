@@ -146,3 +146,71 @@ def test_hsdp_commit_bf16_bitwise():
         assert all(ok for ok, _, _ in res[r]), res[r]
         assert [tot for _, tot, _ in res[r]] == [16, 16, 16]
         assert [w for _, _, w in res[r]] == [2, 1, 1]
+
+
+def _one_replica_worker(rank, world, port, q):
+    """The N=8 shape of configs[1] at any N: one replica per rank, so a
+    replica death is a whole-rank death (the dead rank stops joining
+    barriers; nobody waits on it)."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        from paper_2605_11215_b200.dist import DistributedGradientCommit
+        from oracle import fold
+        g = 4
+        b = world * g
+        numel = 6 * 64 * 29 + 64
+        host = [np.random.default_rng(700 + m).standard_normal(numel).astype(np.float32)
+                for m in range(b)]
+        dev = [torch.from_numpy(h).cuda() for h in host]
+        want = fold.canonical_tree(dict(enumerate(host)), b) / np.float32(b)
+        eng = DistributedGradientCommit(numel, world, g, 6, barrier_timeout_s=20.0)
+
+        class Kill:
+            def __init__(self, plan):
+                self.plan = list(plan)
+
+            def fire(self, phase, bucket=None):
+                hit = [e for e in self.plan if e[0] == phase and (phase != "during_sync" or e[1] == bucket)]
+                self.plan = [e for e in self.plan if e not in hit]
+                return [r for e in hit for r in e[2]]
+
+        res = []
+        for t, plan in enumerate([[], [("during_sync", 3, [1])], [], []]):
+            out = eng.step(t, lambda m, rid: dev[m], Kill(plan))
+            torch.cuda.synchronize()
+            ok = all(eng.grads[r].cpu().numpy().tobytes() == want.tobytes()
+                     for r in eng.comm.members if eng._holds(r))
+            res.append((ok, out.contrib_total, out.w_cur))
+        eng.check_peers()
+        q.put((rank, res))
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_whole_rank_death_one_replica_per_rank():
+    world = min(torch.cuda.device_count(), 4)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = torch.multiprocessing.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_one_replica_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert not isinstance(res[r], str), res[r]
+        assert all(ok for ok, _, _ in res[r]), (r, res[r])
+        assert [tot for _, tot, _ in res[r]] == [4 * world] * 4
+        assert [w for _, _, w in res[r]] == [world] + [world - 1] * 3
