@@ -1585,6 +1585,11 @@ struct rcv_ctx {
     size_t lo, n;
     int variant;
     unsigned long long call;  // bucket call index that combined it
+    // copy-engine all-gather (RCV_CE_GATHER): pull each peer's finished
+    // slice of this bucket from its primary into ours before broadcasting
+    std::vector<std::pair<const char *, std::pair<size_t, size_t>>> gather;  // src base, [a, z)
+    char *dst = nullptr;
+    int es = 4;
   };
   std::vector<Pending> pending;  // combined buckets awaiting the local broadcast
   bool timing = false;
@@ -1615,6 +1620,9 @@ struct rcv_plan {
   int slice_q = 0, slice_nr = 1;
   bool has_bcast = false;
   FoldReq bcast;
+  bool ce_gather = false;             // all-gather by copy engine instead of STG
+  std::vector<const char *> peer_primary;  // per live rank (slice order)
+  char *my_primary = nullptr;
   int variant = 0, comb_variant = 0;
   uint64_t live_mask = 0;
   bool participate = false;
@@ -1652,6 +1660,13 @@ int ctx_flush(rcv_ctx *c, cudaStream_t st, long long upto) {
   while (!c->pending.empty() && (upto < 0 || (long long)c->pending.front().call <= upto)) {
     rcv_ctx::Pending e = c->pending.front();
     c->pending.erase(c->pending.begin());
+    for (auto &g : e.gather) {
+      const size_t a = g.second.first, z = g.second.second;
+      if (z > a)
+        CK(cudaMemcpyAsync(e.dst + (e.lo + a) * e.es, g.first + (e.lo + a) * e.es,
+                           (z - a) * e.es, cudaMemcpyDeviceToDevice, st));
+    }
+    if (e.req.n_out == 0) continue;  // gather only: no other local replica
     shift(e.req, e.lo, e.lo);
     const double bytes = (double)(e.req.n_in + e.req.n_out) * e.n * esize(e.req.acc_dt);
     int rc = timed(c, st, 2, bytes, 0, 0,
@@ -1818,8 +1833,18 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       p->forest_count = k;
     }
   }
+  p->ce_gather = getenv("RCV_CE_GATHER") && atoi(getenv("RCV_CE_GATHER")) && d->participate &&
+                 d->n_comb_out > 1;
+  if (p->ce_gather) {
+    for (int q = 0; q < d->n_comb_out; ++q) p->peer_primary.push_back((const char *)d->comb_out[q]);
+    p->my_primary = (char *)d->comb_out[d->slice_q];
+  }
   if (d->n_comb > 0 && d->participate) {
-    int rc = prepare_tree(d->comb_blocks, d->n_comb, d->n_leaves, d->n_comb_out, d->comb_out,
+    // with the copy-engine gather the combine stores only this rank's slice
+    // into this rank's primary; peers pull it after the next barrier
+    void *const *outs = p->ce_gather ? &d->comb_out[d->slice_q] : d->comb_out;
+    const int n_outs = p->ce_gather ? 1 : d->n_comb_out;
+    int rc = prepare_tree(d->comb_blocks, d->n_comb, d->n_leaves, n_outs, outs,
                           d->acc_dtype, d->divisor, p->comb);
     if (rc) {
       delete p;
@@ -1920,7 +1945,32 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
       if (rc) return rc;
     }
   }
-  if (p->has_bcast) c->pending.push_back({p->bcast, lo, n, p->variant, j});
+  if (p->ce_gather) {
+    rcv_ctx::Pending e;
+    if (p->has_bcast) e.req = p->bcast;  // else n_out stays 0: gather only
+    e.lo = lo;
+    e.n = n;
+    e.variant = p->variant;
+    e.call = j;
+    e.dst = p->my_primary;
+    e.es = es;
+    const size_t units = (n + 63) / 64;
+    for (int q = 0; q < p->slice_nr; ++q) {
+      if (q == p->slice_q) continue;
+      const size_t a = std::min(n, units * q / p->slice_nr * 64);
+      const size_t z = std::min(n, units * (q + 1) / p->slice_nr * 64);
+      e.gather.push_back({p->peer_primary[q], {a, z}});
+    }
+    c->pending.push_back(e);
+  } else if (p->has_bcast) {
+    rcv_ctx::Pending e;
+    e.req = p->bcast;
+    e.lo = lo;
+    e.n = n;
+    e.variant = p->variant;
+    e.call = j;
+    c->pending.push_back(e);
+  }
   return RCV_OK;
 }
 
