@@ -1,7 +1,7 @@
 #!/bin/bash
 # GPU-box job: parity tests, smoke, bench, then (only if the bench exited 0)
 # the ncu launch list and one full capture of the dominant kernel.
-# usage: bash gpu_check.sh TAG [bench args...]
+# usage: bash tools/gpu_check.sh TAG [bench args...]
 TAG=${1:-r1}; shift
 OUT=gpurun_out; mkdir -p $OUT
 timeout 900 python -m pytest tests -m gpu -q -x > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?" | tee -a $OUT/pytest_gpu_$TAG.log

@@ -19,7 +19,7 @@ import sys
 import torch
 import torch.distributed as dist
 
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 D_LLAMA_1B = 1_235_814_400
 TOKENS_PER_MB = 4096

@@ -10,7 +10,7 @@ import sys
 import torch
 import torch.distributed as dist
 
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_11215_b200 import _lib  # noqa: E402
 from paper_2605_11215_b200.dist import PeerBuffers  # noqa: E402
 

@@ -3,7 +3,7 @@ import os, sys, time
 import numpy as np
 import torch
 import torch.distributed as dist
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 def log(*a):
     print("[rank %s %.2f]" % (os.environ.get("RANK"), time.time() % 1000), *a, file=sys.stderr, flush=True)
@@ -12,7 +12,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "--spawn":
     # plain launcher: torchrun's agent would SIGTERM the survivors
     import subprocess
     n = int(sys.argv[2])
-    ps = [subprocess.Popen([sys.executable, __file__], env=dict(os.environ, RANK=str(r), LOCAL_RANK=str(r),
+    ps = [subprocess.Popen([sys.executable, os.path.abspath(__file__)], env=dict(os.environ, RANK=str(r), LOCAL_RANK=str(r),
           WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT="29544")) for r in range(n)]
     for p in ps:
         try:

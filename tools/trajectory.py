@@ -22,7 +22,7 @@ import time
 os.environ.setdefault("CUBLAS_WORKSPACE_CONFIG", ":4096:8")
 import torch  # noqa: E402
 
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_11215_b200.executor import (CanonicalExecutor, TinyTransformer,  # noqa: E402
                                             lm_loss, synthetic_lm_batch)
 
