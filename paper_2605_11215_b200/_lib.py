@@ -377,23 +377,6 @@ def barrier(local_flags: torch.Tensor, peer_flag_ptrs: Sequence[int], me: int,
                               stream_of(local_flags)))
 
 
-def tree_commit_raw(blocks: Sequence[tuple], n_leaves: int,
-                    out_ptrs: Sequence[int], numel: int, acc_dtype: int,
-                    divisor: float, stream: int,
-                    variant: int = VARIANT_AUTO) -> None:
-    """tree_commit over raw device pointers (peer-mapped allowed):
-    blocks = [(ptr, lo, level, dtype)], ascending lo."""
-    if not out_ptrs or numel == 0:
-        return
-    arr = (_Block * max(1, len(blocks)))()
-    for i, (ptr, lo, level, dt) in enumerate(blocks):
-        arr[i] = _Block(ptr, lo, level, dt)
-    outs = (ctypes.c_void_p * len(out_ptrs))(*out_ptrs)
-    _check(load().rcv_tree_commit(arr, len(blocks), n_leaves, len(out_ptrs),
-                                  outs, acc_dtype, numel, float(divisor),
-                                  variant, stream))
-
-
 class TreePlan:
     """Prebuilt pointer arrays for repeated rcv_tree_commit_at calls: one
     plan per (cover, outputs), then one cheap call per bucket or slice.

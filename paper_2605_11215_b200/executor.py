@@ -20,7 +20,7 @@ optimizer's gradient.
 
 from __future__ import annotations
 
-from typing import Callable, Dict, List, Optional, Tuple
+from typing import Callable, Dict, List, Tuple
 
 import torch
 import torch.nn as nn
@@ -29,8 +29,8 @@ from .commit import CommitOutcome, GradientCommit
 
 
 def flatten_module(module: nn.Module, device) -> Tuple[torch.Tensor, List[torch.Tensor]]:
-    """Move every parameter of `module` into one flat fp32 buffer; returns
-    (flat, views) with the module's parameters now views of `flat`."""
+    """Move every trainable parameter of `module` into one flat fp32 buffer;
+    returns (flat, params) with each parameter's data now a view of `flat`."""
     params = [p for p in module.parameters() if p.requires_grad]
     numel = sum(p.numel() for p in params)
     flat = torch.empty(numel, dtype=torch.float32, device=device)

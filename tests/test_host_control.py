@@ -13,7 +13,7 @@ from paper_2605_11215_b200.policy import (
     InvariantViolation, adaptive_policy_adjustment, assign_roles,
     boundary_minor_count, contribution_quota, extension_rounds, initial_state,
     policy_adjustment, policy_advancement)
-from oracle.protocol import ext_rounds, layout
+from oracle.protocol import layout
 
 M, MI, MS, NS, BM = (ReplicaRole.MAJOR, ReplicaRole.MINOR, ReplicaRole.MAJOR_SPARE,
                      ReplicaRole.MINOR_SPARE, ReplicaRole.BOUNDARY_MINOR)

@@ -13,7 +13,6 @@ quota is redistributed to the survivor.  One JSON line (rank 0).
 import argparse
 import json
 import os
-import statistics
 import sys
 
 import torch
