@@ -181,7 +181,9 @@ int rcv_unit_lanes(double *out, uint64_t base, size_t n, double scale,
  *   linear:   r = params.x - y ; grad = r * x ; loss = r * r
  *   constant: grad = x         ; loss = params.x
  * where x = lanes[0:dim], and for linear y = wstar.x + 0.1*lanes[dim]
- * (trainer.py:165-168).  Dot products are a fixed-order sequential fold.
+ * (trainer.py:165-168).  Dot products are a fixed-order multi-block fold
+ * (deterministic for a given dim). scal must hold 2 + 1024 doubles (the
+ * block partials follow the two results).
  * grad (dim doubles; may be NULL to compute the loss only) and scal (two
  * doubles: scal[0] = r for linear / 1.0 for constant, scal[1] = loss) are
  * device outputs. */

@@ -588,39 +588,57 @@ __global__ void unit_lanes_kernel(double *out, uint64_t base,
   }
 }
 
-// Fixed-order dot products: TOY_T threads each fold a contiguous chunk in
-// index order, then thread 0 folds the chunk sums in thread order.
+// Fixed-order dot products over many blocks: block b owns a contiguous chunk,
+// thread t folds the chunk's elements t, t+TOY_T, ... in order, the block
+// folds its threads in a fixed tree, and one thread folds the block partials
+// in block order.  Deterministic for a given dim; not numpy's ddot order, so
+// the linear toy model is compared within tolerance (the constant model's
+// integer data is exact either way).
 #define TOY_T 256
-__global__ void toy_dot_kernel(int linear, const double *params,
-                               const double *lanes, const double *wstar,
-                               unsigned long long dim, double *scal) {
-  __shared__ double part_p[TOY_T], part_w[TOY_T];
-  const unsigned long long chunk = (dim + TOY_T - 1) / TOY_T;
-  const unsigned long long lo = threadIdx.x * chunk;
+#define TOY_MAXB 512
+__global__ void toy_dot_partial_kernel(int linear, const double *params,
+                                       const double *lanes, const double *wstar,
+                                       unsigned long long dim, unsigned long long chunk,
+                                       double *part) {
+  __shared__ double sp_s[TOY_T], sw_s[TOY_T];
+  const unsigned long long lo = blockIdx.x * chunk;
   const unsigned long long hi = min(dim, lo + chunk);
   double sp = 0.0, sw = 0.0;
-  for (unsigned long long i = lo; i < hi; ++i) {
+  for (unsigned long long i = lo + threadIdx.x; i < hi; i += TOY_T) {
     sp = __dadd_rn(sp, __dmul_rn(params[i], lanes[i]));
     if (linear) sw = __dadd_rn(sw, __dmul_rn(wstar[i], lanes[i]));
   }
-  part_p[threadIdx.x] = sp;
-  part_w[threadIdx.x] = sw;
+  sp_s[threadIdx.x] = sp;
+  sw_s[threadIdx.x] = sw;
   __syncthreads();
+  for (int w = TOY_T / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      sp_s[threadIdx.x] = __dadd_rn(sp_s[threadIdx.x], sp_s[threadIdx.x + w]);
+      sw_s[threadIdx.x] = __dadd_rn(sw_s[threadIdx.x], sw_s[threadIdx.x + w]);
+    }
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
-    double tp = 0.0, tw = 0.0;
-    for (int t = 0; t < TOY_T; ++t) {
-      tp = __dadd_rn(tp, part_p[t]);
-      tw = __dadd_rn(tw, part_w[t]);
-    }
-    if (linear) {
-      const double y = __dadd_rn(tw, __dmul_rn(0.1, lanes[dim]));
-      const double r = __dsub_rn(tp, y);
-      scal[0] = r;               // residual
-      scal[1] = __dmul_rn(r, r); // loss
-    } else {
-      scal[0] = 1.0;
-      scal[1] = tp;
-    }
+    part[2 * blockIdx.x] = sp_s[0];
+    part[2 * blockIdx.x + 1] = sw_s[0];
+  }
+}
+
+__global__ void toy_finalize_kernel(int linear, const double *lanes, unsigned long long dim,
+                                    const double *part, int nb, double *scal) {
+  double tp = 0.0, tw = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    tp = __dadd_rn(tp, part[2 * b]);
+    tw = __dadd_rn(tw, part[2 * b + 1]);
+  }
+  if (linear) {
+    const double y = __dadd_rn(tw, __dmul_rn(0.1, lanes[dim]));
+    const double r = __dsub_rn(tp, y);
+    scal[0] = r;               // residual
+    scal[1] = __dmul_rn(r, r); // loss
+  } else {
+    scal[0] = 1.0;
+    scal[1] = tp;
   }
 }
 
@@ -1548,8 +1566,16 @@ int rcv_toy_grad(int kind_linear, const double *params, const double *lanes,
                  const double *wstar, size_t dim, double *grad, double *scal,
                  void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  // block partials live in scal[2..]: the caller's scratch holds 2 + 2*TOY_MAXB doubles
+  const unsigned long long nb = std::max<unsigned long long>(
+      1, std::min<unsigned long long>(TOY_MAXB, (dim + 4095) / 4096));
+  const unsigned long long chunk = (dim + nb - 1) / nb;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  toy_dot_kernel<<<1, TOY_T, 0, st>>>(kind_linear, params, lanes, wstar, dim, scal);
+  toy_dot_partial_kernel<<<(unsigned)nb, TOY_T, 0, st>>>(kind_linear, params, lanes, wstar, dim,
+                                                          chunk, scal + 2);
+  CK(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  toy_finalize_kernel<<<1, 1, 0, st>>>(kind_linear, lanes, dim, scal + 2, (int)nb, scal);
   CK(cudaGetLastError());
   if (dim && grad) {  // grad == NULL: loss only (the constant stream's x is g0)
     const int sms = current_device_sms();
