@@ -1722,7 +1722,14 @@ int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer
   c->bar.timeout_ns = timeout_ns;
   c->bar.n = n_ranks;
   c->bar.me = me;
-  CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  // the side stream carries the HBM-bound critical path (pre-reduce and
+  // local broadcast); RCV_SIDE_PRIORITY=1 schedules its CTAs ahead of the
+  // NVLink-bound combine on the caller's stream
+  int lo_pri = 0, hi_pri = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+  const char *sp = getenv("RCV_SIDE_PRIORITY");
+  CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking,
+                                  (sp && atoi(sp)) ? hi_pri : lo_pri));
   CK(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
   for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->ev_arrived[i], cudaEventDisableTiming));
