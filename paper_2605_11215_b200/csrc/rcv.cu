@@ -34,6 +34,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <atomic>
 #include <mutex>
 #include <string>
@@ -70,14 +71,31 @@ static int set_err(int code, const char *fmt, ...) {
 // ---------------------------------------------------------------------------
 // device helpers
 
+// fp32 accumulation over bf16 inputs works on 8-element vectors so that a bf16
+// input vector is one 16-byte load (8 elements) like every other access
+struct __align__(16) float8 {
+  float4 a, b;
+};
+struct F8 {};  // accumulator tag: fp32, 8 elements per vector
+
 template <typename A> struct VecT;
 template <> struct VecT<float> {
   using V = float4;
   static constexpr int E = 4;  // elements per 16-byte vector
+  static constexpr int OUT = 16;
+  __host__ __device__ static constexpr int in_bytes(bool bf16) { return bf16 ? 8 : 16; }
 };
 template <> struct VecT<double> {
   using V = double2;
   static constexpr int E = 2;
+  static constexpr int OUT = 16;
+  __host__ __device__ static constexpr int in_bytes(bool) { return 16; }
+};
+template <> struct VecT<F8> {
+  using V = float8;
+  static constexpr int E = 8;
+  static constexpr int OUT = 32;
+  __host__ __device__ static constexpr int in_bytes(bool bf16) { return bf16 ? 16 : 32; }
 };
 
 __device__ __forceinline__ float4 vadd(const float4 &a, const float4 &b) {
@@ -101,12 +119,22 @@ __device__ __forceinline__ float4 vdiv(const float4 &a, double d) {
 __device__ __forceinline__ double2 vdiv(const double2 &a, double d) {
   return make_double2(__ddiv_rn(a.x, d), __ddiv_rn(a.y, d));
 }
+__device__ __forceinline__ float8 vadd(const float8 &x, const float8 &y) {
+  return float8{vadd(x.a, y.a), vadd(x.b, y.b)};
+}
+__device__ __forceinline__ float8 vcanon(const float8 &x) { return float8{vcanon(x.a), vcanon(x.b)}; }
+__device__ __forceinline__ float8 vdiv(const float8 &x, double d) {
+  return float8{vdiv(x.a, d), vdiv(x.b, d)};
+}
 template <typename V> __device__ __forceinline__ V vzero();
 template <> __device__ __forceinline__ float4 vzero<float4>() {
   return make_float4(0.f, 0.f, 0.f, 0.f);
 }
 template <> __device__ __forceinline__ double2 vzero<double2>() {
   return make_double2(0.0, 0.0);
+}
+template <> __device__ __forceinline__ float8 vzero<float8>() {
+  return float8{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
 }
 
 // 4 bf16 (8 bytes) -> float4, exact widening
@@ -123,7 +151,23 @@ __device__ __forceinline__ float4 bf16x4_to_f4(uint2 raw) {
 template <typename A>
 __device__ __forceinline__ typename VecT<A>::V ld_vec(const char *p,
                                                       bool bf16) {
-  if constexpr (sizeof(A) == 4) {
+  if constexpr (std::is_same<A, F8>::value) {
+    if (bf16) {  // 8 bf16 in one 16-byte load
+      uint4 raw;
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
+                   : "l"(p));
+      return float8{bf16x4_to_f4(make_uint2(raw.x, raw.y)), bf16x4_to_f4(make_uint2(raw.z, raw.w))};
+    }
+    float8 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.a.x), "=f"(v.a.y), "=f"(v.a.z), "=f"(v.a.w)
+                 : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.b.x), "=f"(v.b.y), "=f"(v.b.z), "=f"(v.b.w)
+                 : "l"(p + 16));
+    return v;
+  } else if constexpr (sizeof(A) == 4) {
     if (bf16) {
       uint2 raw;
       asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
@@ -148,7 +192,13 @@ __device__ __forceinline__ typename VecT<A>::V ld_vec(const char *p,
 template <typename A>
 __device__ __forceinline__ typename VecT<A>::V lds_vec(const unsigned char *p,
                                                        bool bf16) {
-  if constexpr (sizeof(A) == 4) {
+  if constexpr (std::is_same<A, F8>::value) {
+    if (bf16) {
+      const uint4 raw = *reinterpret_cast<const uint4 *>(p);
+      return float8{bf16x4_to_f4(make_uint2(raw.x, raw.y)), bf16x4_to_f4(make_uint2(raw.z, raw.w))};
+    }
+    return float8{*reinterpret_cast<const float4 *>(p), *reinterpret_cast<const float4 *>(p + 16)};
+  } else if constexpr (sizeof(A) == 4) {
     if (bf16) return bf16x4_to_f4(*reinterpret_cast<const uint2 *>(p));
     return *reinterpret_cast<const float4 *>(p);
   } else {
@@ -158,6 +208,10 @@ __device__ __forceinline__ typename VecT<A>::V lds_vec(const unsigned char *p,
 
 template <typename V> __device__ __forceinline__ void st_vec(char *p, const V &v) {
   *reinterpret_cast<V *>(p) = v;
+}
+__device__ __forceinline__ void st_vec(char *p, const float8 &v) {
+  *reinterpret_cast<float4 *>(p) = v.a;
+  *reinterpret_cast<float4 *>(p + 16) = v.b;
 }
 
 // Fixed-capacity register stack.  Indices are compared against the (warp-
@@ -347,9 +401,9 @@ __global__ void __launch_bounds__(256)
        v < p.nvec; v += (unsigned long long)gridDim.x * blockDim.x) {
     auto ld = [&](int i) {
       const bool b = p.bf16[i];
-      return ld_vec<A>(p.in[i] + v * (b ? 8ull : 16ull), b);
+      return ld_vec<A>(p.in[i] + v * (unsigned long long)VecT<A>::in_bytes(b), b);
     };
-    emit<Prog, V>(p, ld, v * 16ull);
+    emit<Prog, V>(p, ld, v * (unsigned long long)VecT<A>::OUT);
   }
 }
 
@@ -431,11 +485,11 @@ __global__ void __launch_bounds__(TMA_THREADS)
         const unsigned long long v0 = t * tv;
         const uint32_t nv = (uint32_t)min(tv, p.nvec - v0);
         uint32_t total = 0;
-        for (int i = 0; i < p.n_in; ++i) total += nv * (p.bf16[i] ? 8u : 16u);
+        for (int i = 0; i < p.n_in; ++i) total += nv * (uint32_t)VecT<A>::in_bytes(p.bf16[i]);
         mbar_expect_tx(&full[s], total);
         unsigned char *stage = smem + (size_t)s * p.stage_bytes;
         for (int i = 0; i < p.n_in; ++i) {
-          const uint32_t vb = p.bf16[i] ? 8u : 16u;
+          const uint32_t vb = (uint32_t)VecT<A>::in_bytes(p.bf16[i]);
           bulk_g2s(stage + p.smem_off[i], p.in[i] + v0 * vb, nv * vb, &full[s]);
         }
         if (++s == p.stages) {
@@ -460,9 +514,9 @@ __global__ void __launch_bounds__(TMA_THREADS)
       if (vi >= nv) break;
       auto ld = [&](int i) {
         const bool b = p.bf16[i];
-        return lds_vec<A>(stage + p.smem_off[i] + (size_t)vi * (b ? 8 : 16), b);
+        return lds_vec<A>(stage + p.smem_off[i] + (size_t)vi * VecT<A>::in_bytes(b), b);
       };
-      emit<Prog, V>(p, ld, (v0 + vi) * 16ull);
+      emit<Prog, V>(p, ld, (v0 + vi) * (unsigned long long)VecT<A>::OUT);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -815,7 +869,7 @@ void fill_vec_params(FoldParams &p, const FoldReq &r, unsigned long long e0,
     p.op[i] = r.op[i];
     p.bf16[i] = r.in_dt[i] == RCV_BF16;
   }
-  for (int j = 0; j < r.n_out; ++j) p.out[j] = r.out[j] + e0 * sizeof(A);
+  for (int j = 0; j < r.n_out; ++j) p.out[j] = r.out[j] + e0 * esize(r.acc_dt);
   p.nvec = nvec;
   p.divisor = r.divisor;
   p.guard = r.guard;
@@ -851,9 +905,10 @@ struct TmaGeom {
   size_t smem;
 };
 
+template <typename A>
 bool tma_geom(const FoldReq &r, TmaGeom *g) {
   uint32_t bytes_per_vec = 0;  // sum over inputs of one vector
-  for (int i = 0; i < r.n_in; ++i) bytes_per_vec += r.in_dt[i] == RCV_BF16 ? 8 : 16;
+  for (int i = 0; i < r.n_in; ++i) bytes_per_vec += VecT<A>::in_bytes(r.in_dt[i] == RCV_BF16);
   const uint32_t per_vpt = bytes_per_vec * TMA_CONSUMERS;  // stage bytes at vpt=1
   int vpt = 1;
   while (vpt < 8 && per_vpt * (vpt * 2) <= 32768) vpt *= 2;
@@ -881,7 +936,7 @@ int launch_tma_p(const FoldReq &r, const TmaGeom &g, unsigned long long e0,
   uint32_t off = 0;
   for (int i = 0; i < r.n_in; ++i) {
     p.smem_off[i] = off;
-    off += (uint32_t)TMA_CONSUMERS * g.vpt * (p.bf16[i] ? 8u : 16u);
+    off += (uint32_t)TMA_CONSUMERS * g.vpt * (uint32_t)VecT<A>::in_bytes(p.bf16[i]);
   }
   p.stage_bytes = g.stage_bytes;
   p.stages = g.stages;
@@ -973,7 +1028,9 @@ int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int s
     return RCV_OK;
   }
   const bool f64 = r.acc_dt == RCV_F64;
-  const int E = f64 ? 2 : 4;
+  bool wide = false;  // fp32 over bf16 inputs: 8-element vectors (float8)
+  for (int i = 0; i < r.n_in && !f64; ++i) wide |= r.in_dt[i] == RCV_BF16;
+  const int E = f64 ? 2 : (wide ? 8 : 4);
   int h = variant == RCV_VARIANT_SCALAR ? -1 : common_head(r);
   if (r.n_roots > 0 && (h != 0 || (numel % (2 * E)) != 0))
     return set_err(RCV_EINVAL, "forest fold needs 16-byte aligned, vector-multiple ranges");
@@ -997,13 +1054,15 @@ int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int s
     // ring, which decouples their loads from the control flow.
     if (variant == RCV_VARIANT_AUTO && (r.full_L >= 0 || r.n_roots > 0)) variant = RCV_VARIANT_DIRECT;
     bool use_tma = variant == RCV_VARIANT_TMA || variant == RCV_VARIANT_AUTO;
-    if (use_tma && !tma_geom(r, &g)) {
+    const bool geom_ok = f64 ? tma_geom<double>(r, &g) : (wide ? tma_geom<F8>(r, &g) : tma_geom<float>(r, &g));
+    if (use_tma && !geom_ok) {
       if (variant == RCV_VARIANT_TMA)
         return set_err(RCV_EINVAL, "TMA variant: %d inputs do not fit a 2-stage ring", r.n_in);
       use_tma = false;
     }
     rc = f64 ? launch_vec<double>(r, use_tma, g, maxd, h, nvec, st, sms)
-             : launch_vec<float>(r, use_tma, g, maxd, h, nvec, st, sms);
+             : (wide ? launch_vec<F8>(r, use_tma, g, maxd, h, nvec, st, sms)
+                     : launch_vec<float>(r, use_tma, g, maxd, h, nvec, st, sms));
     if (rc) return rc;
   }
   if (body_end < numel) {

@@ -238,3 +238,23 @@ def test_multidevice_allreduce():
         for v in views:
             torch.cuda.synchronize(v.device)
             assert host(v).tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("variant", [_lib.VARIANT_AUTO, _lib.VARIANT_TMA, _lib.VARIANT_DIRECT])
+def test_bf16_leaves_wide_path(variant):
+    """fp32 commit of bf16 microbatch gradients (HSDP shard leaves): 8-wide
+    vectors, every load 16 bytes; bitwise vs the oracle on the widened data,
+    including misaligned starts and ragged tails."""
+    rng = np.random.default_rng(21)
+    for n_leaves, numel, off in ((8, 4099, 0), (32, 50001, 3), (5, 777, 1), (16, 1 << 16, 8)):
+        raw = [torch.from_numpy(rng.standard_normal(numel + off).astype(np.float32)).to(torch.bfloat16)
+               for _ in range(n_leaves)]
+        views = [r.to(DEV)[off:] for r in raw]
+        widened = {m: r[off:].float().numpy() for m, r in enumerate(raw)}
+        width = 1 << max(0, (n_leaves - 1).bit_length())
+        want = fold.canonical_tree(widened, width) / np.float32(n_leaves)
+        outs = [torch.empty(numel + off, dtype=torch.float32, device=DEV)[off:] for _ in range(2)]
+        _lib.tree_commit([(v, m, 0) for m, v in enumerate(views)], width, outs,
+                         float(n_leaves), variant=variant)
+        for o in outs:
+            assert host(o).tobytes() == want.tobytes(), (variant, n_leaves, numel, off)
