@@ -518,10 +518,26 @@ def e2e_leg(args, dev, leaves, numel, world=1):
 
 def main():
     args = parse()
-    if args.impl == "reference":
-        run_reference_arm(args)
-    else:
-        run_ours(args)
+    # exactly one JSON line on stdout: libraries (NCCL's version banner at
+    # lazy communicator init) print to fd 1, so route fd 1 to stderr and keep
+    # a private descriptor for the result line
+    out_fd = os.dup(1)
+    os.dup2(2, 1)
+    global print
+    builtin_print = print
+
+    def print(*a, **k):  # noqa: A001 - the result line goes to the saved stdout
+        if a and isinstance(a[0], str) and a[0].startswith("{"):
+            os.write(out_fd, (a[0] + "\n").encode())
+        else:
+            builtin_print(*a, **k)
+    try:
+        if args.impl == "reference":
+            run_reference_arm(args)
+        else:
+            run_ours(args)
+    finally:
+        sys.stdout.flush()
 
 
 if __name__ == "__main__":
