@@ -258,3 +258,40 @@ def test_bf16_leaves_wide_path(variant):
                          float(n_leaves), variant=variant)
         for o in outs:
             assert host(o).tobytes() == want.tobytes(), (variant, n_leaves, numel, off)
+
+
+def _random_program(rng, n):
+    """A random valid stack program over n inputs (include/rcv.h): after
+    each push merge 0..(depth-1) times, ending with one value; depth <= 8."""
+    ops, depth = [], 0
+    for i in range(n):
+        depth += 1
+        last = i == n - 1
+        if last:
+            m = depth - 1
+        else:
+            m = int(rng.integers(0, depth))
+            if depth - m > 7:              # keep within ProgStack<8>
+                m = depth - 7
+        depth -= m
+        op = m | (0x40 if rng.random() < 0.2 else 0)
+        ops.append(op)
+    return ops
+
+
+@pytest.mark.parametrize("variant", [_lib.VARIANT_AUTO, _lib.VARIANT_TMA, _lib.VARIANT_DIRECT, _lib.VARIANT_SCALAR])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_random_stack_programs(variant, dtype):
+    rng = np.random.default_rng(17 + (dtype == torch.float64))
+    for trial in range(12):
+        n = int(rng.integers(1, 40))
+        numel = int(rng.integers(1, 9000))
+        ops = _random_program(rng, n)
+        xs = [rng.standard_normal(numel).astype(NP_DT[dtype]) for _ in range(n)]
+        for x in xs:
+            x[rng.integers(0, numel, size=min(2, numel))] = -0.0
+        div = float(rng.choice([0.0, 3.0, 7.0]))
+        want = fold.run_program(xs, ops, divisor=div)
+        out = torch.empty(numel, dtype=dtype, device=DEV)
+        _lib.fold([dev(x) for x in xs], ops, [out], divisor=div, variant=variant)
+        assert host(out).tobytes() == want.tobytes(), (variant, trial, ops)
