@@ -247,7 +247,7 @@ int rcv_ctx_finish(rcv_ctx *ctx, uint64_t live_mask, int participate,
                    void *main_stream);
 int rcv_ctx_set_timing(rcv_ctx *ctx, int on);
 /* Drain recorded launch timings (call after synchronising): up to `max`
- * entries of kind (0 pre-reduce, 1 barrier, 2 broadcast, 3 combine),
+ * entries of kind (0 pre-reduce, 1 barrier, 2 broadcast, 3 combine, 4 fused),
  * milliseconds, algorithmic HBM bytes, NVLink in / out bytes. */
 int rcv_ctx_timing(rcv_ctx *ctx, int max, int *kind, float *ms, double *bytes,
                    double *nvl_in, double *nvl_out, int *count);
@@ -276,6 +276,10 @@ typedef struct {
   int remote_in, remote_out;     /* NVLink accounting of the combine */
   int guarded;                   /* real-kill mode: skip the combine once a
                                     live peer timed out (status word) */
+  int fused;                     /* one fused pre-reduce+combine kernel per
+                                    bucket (every live rank must agree; needs
+                                    fp32, <= 8 perfect local nodes, <= 64
+                                    local leaves, n_leaves <= 64) */
 } rcv_plan_desc;
 
 int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *desc, rcv_plan **out);

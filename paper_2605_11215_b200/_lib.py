@@ -62,7 +62,7 @@ class PlanDesc(ctypes.Structure):
         ("variant", ctypes.c_int), ("comb_variant", ctypes.c_int),
         ("live_mask", ctypes.c_uint64), ("participate", ctypes.c_int),
         ("remote_in", ctypes.c_int), ("remote_out", ctypes.c_int),
-        ("guarded", ctypes.c_int),
+        ("guarded", ctypes.c_int), ("fused", ctypes.c_int),
     ]
 
 
@@ -405,7 +405,7 @@ class TreePlan:
                        self.variant, stream))
 
 
-KIND_NAMES = ("prereduce", "barrier", "broadcast", "combine")
+KIND_NAMES = ("prereduce", "barrier", "broadcast", "combine", "fused")
 
 
 class BucketRuntime:

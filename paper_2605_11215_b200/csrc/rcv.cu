@@ -119,6 +119,8 @@ __device__ __forceinline__ float4 vdiv(const float4 &a, double d) {
 __device__ __forceinline__ double2 vdiv(const double2 &a, double d) {
   return make_double2(__ddiv_rn(a.x, d), __ddiv_rn(a.y, d));
 }
+__device__ __forceinline__ float vadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float vcanon(float a) { return __fadd_rn(0.f, a); }
 __device__ __forceinline__ float8 vadd(const float8 &x, const float8 &y) {
   return float8{vadd(x.a, y.a), vadd(x.b, y.b)};
 }
@@ -133,6 +135,7 @@ template <> __device__ __forceinline__ float4 vzero<float4>() {
 template <> __device__ __forceinline__ double2 vzero<double2>() {
   return make_double2(0.0, 0.0);
 }
+template <> __device__ __forceinline__ float vzero<float>() { return 0.f; }
 template <> __device__ __forceinline__ float8 vzero<float8>() {
   return float8{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
 }
@@ -271,8 +274,8 @@ struct FoldParams {
 
 // Generic: the stack program of include/rcv.h (push; merge top two).
 template <int MAXD> struct ProgStack {
-  template <typename V, typename Ld>
-  __device__ __forceinline__ static V eval(const FoldParams &p, const Ld &ld) {
+  template <typename V, typename Ld, typename P = FoldParams>
+  __device__ __forceinline__ static V eval(const P &p, const Ld &ld) {
     Stack<MAXD, V> st;
     for (int i = 0; i < p.n_in; ++i) {
       V x = ld(i);
@@ -288,8 +291,8 @@ template <int MAXD> struct ProgStack {
 // Left fold ((x0 + x1) + x2) + ...: the reference collective's order
 // (comm.py:192-196) and the accumulation `flat += grad` (trainer.py:212).
 struct ProgLeft {
-  template <typename V, typename Ld>
-  __device__ __forceinline__ static V eval(const FoldParams &p, const Ld &ld) {
+  template <typename V, typename Ld, typename P = FoldParams>
+  __device__ __forceinline__ static V eval(const P &p, const Ld &ld) {
     V acc = ld(0);
     if (p.op[0] & RCV_OP_CANON) acc = vcanon(acc);
     for (int i = 1; i < p.n_in; ++i) acc = vadd(acc, ld(i));
@@ -301,8 +304,8 @@ struct ProgLeft {
 // input when one feeds it, else left + right when both subtrees hold
 // something, else the non-empty side (empty leaves are skipped, not zeros).
 template <int L> struct ProgTree {
-  template <int LEVEL, int IDX, typename V, typename Ld>
-  __device__ __forceinline__ static bool node(const FoldParams &p, const Ld &ld, V &out) {
+  template <int LEVEL, int IDX, typename V, typename Ld, typename P>
+  __device__ __forceinline__ static bool node(const P &p, const Ld &ld, V &out) {
     constexpr int id = (1 << (L - LEVEL)) - 1 + IDX;
     if (!p.present[id]) return false;
     const int in = p.node_in[id];
@@ -318,8 +321,8 @@ template <int L> struct ProgTree {
     }
     return true;
   }
-  template <typename V, typename Ld>
-  __device__ __forceinline__ static V eval(const FoldParams &p, const Ld &ld) {
+  template <typename V, typename Ld, typename P = FoldParams>
+  __device__ __forceinline__ static V eval(const P &p, const Ld &ld) {
     V r = vzero<V>();
     node<L, 0>(p, ld, r);
     return r;
@@ -340,8 +343,8 @@ template <int L> struct ProgFull {
       return vadd(a, b);
     }
   }
-  template <typename V, typename Ld>
-  __device__ __forceinline__ static V eval(const FoldParams &, const Ld &ld) {
+  template <typename V, typename Ld, typename P = FoldParams>
+  __device__ __forceinline__ static V eval(const P &, const Ld &ld) {
     return node<L, 0, V>(ld);
   }
 };
@@ -351,8 +354,8 @@ template <int L> struct ProgFull {
 // output, without the divisor (pre-reduce partials).
 struct ProgForest {
   static constexpr bool kMulti = true;
-  template <typename V, typename Ld, typename St>
-  __device__ __forceinline__ static void run(const FoldParams &p, const Ld &ld, const St &st) {
+  template <typename V, typename Ld, typename St, typename P = FoldParams>
+  __device__ __forceinline__ static void run(const P &p, const Ld &ld, const St &st) {
     for (int f = 0; f < p.n_roots; ++f) {
       const int base = p.root_first[f];
       auto sub = [&](int i) { return ld(base + i); };
@@ -750,6 +753,152 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   }
   __syncthreads();
   __threadfence_system();
+}
+
+// ---------------------------------------------------------------------------
+// fused bucket kernel (multi-process): local pre-reduce and the owner-slice
+// combine in ONE launch, synchronised per owner slice by release/acquire
+// flags in peer memory instead of a barrier kernel between two launches.
+//
+//   CTAs [0, a_ctas)   phase A: the rank's cover nodes (a forest of perfect
+//                      trees over its local leaves) into its pool slots,
+//                      slice by slice in owner order; the last CTA to finish
+//                      slice q releases `seq` into owner q's ready[me] flag.
+//   CTAs [a_ctas, ..)  phase B: acquire ready[p] >= seq from every producer
+//                      p (bounded by %globaltimer), then fold this rank's
+//                      slice over every node's partial (peers' over NVLink),
+//                      divide, and store it into every live rank's primary.
+//
+// Phase-A CTAs never wait and the grid never exceeds one CTA per SM, so all
+// CTAs are co-resident and the kernel cannot deadlock on its own GPU; a
+// producer that stops responding times out into the status word and the
+// combine is skipped (real-kill mode).
+
+#define FUSED_T 256
+#define FUSED_MAX_SLICES 32
+
+struct FusedParams {
+  // phase A
+  const char *leaf[RCV_MAX_IN];
+  int n_leaf;
+  int n_roots;
+  uint8_t root_L[8];
+  uint8_t root_first[8];
+  char *pool_out[8];
+  // phase B
+  const char *node[RCV_MAX_IN];
+  int n_node;
+  int8_t node_in[2 * RCV_MAX_IN - 1];
+  uint8_t present[2 * RCV_MAX_IN - 1];
+  char *out[FUSED_MAX_SLICES];
+  int n_out;
+  double divisor;
+  unsigned long long slice_lo[FUSED_MAX_SLICES + 1];  // in vectors
+  int n_slices;
+  int my_slice;
+  unsigned long long *ready_out[FUSED_MAX_SLICES];     // owner q's ready array
+  unsigned long long *ready_in;
+  unsigned int producers;  // rank bits this rank's combine waits for
+  unsigned int guard_mask;
+  int me;
+  unsigned long long seq;
+  unsigned int *counter;   // device-local, one per slice
+  unsigned int *status;
+  unsigned long long timeout_ns;
+  int a_ctas;
+  int tail;  // n mod 4 trailing elements, handled by scalar code
+};
+
+// coherent 16-byte load (the pool slot was written during this kernel, on
+// this or another GPU): bypass L1, no read-only path
+__device__ __forceinline__ float4 ld_cg_f4(const char *p) {
+  float4 v;
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+template <typename ProgB>
+__global__ void __launch_bounds__(FUSED_T, 4)
+    fused_bucket_kernel(const __grid_constant__ FusedParams p) {
+  const int tid = threadIdx.x;
+  if ((int)blockIdx.x < p.a_ctas) {
+    // ---- phase A: local partials, slice by slice in owner order ----
+    const int a = blockIdx.x;
+    for (int q = 0; q < p.n_slices; ++q) {
+      for (unsigned long long v = p.slice_lo[q] + (unsigned long long)a * FUSED_T + tid;
+           v < p.slice_lo[q + 1]; v += (unsigned long long)p.a_ctas * FUSED_T) {
+        auto ld = [&](int i) { return ld_vec<float>(p.leaf[i] + v * 16ull, false); };
+        ProgForest::run<float4>(p, ld, [&](int f, float4 r) { st_vec(p.pool_out[f] + v * 16ull, r); });
+      }
+      if (q == p.n_slices - 1 && a == 0 && tid < p.tail) {  // ragged end: scalar
+        const unsigned long long e = p.slice_lo[p.n_slices] * 4ull + tid;
+        auto ld = [&](int i) { return reinterpret_cast<const float *>(p.leaf[i])[e]; };
+        ProgForest::run<float>(p, ld, [&](int f, float r) {
+          reinterpret_cast<float *>(p.pool_out[f])[e] = r;
+        });
+      }
+      __threadfence_system();  // this thread's partial stores, before the count
+      __syncthreads();
+      if (tid == 0) {
+        const unsigned int done = atomicAdd(&p.counter[q], 1u) + 1u;
+        if (done == (unsigned int)p.a_ctas) {  // the slice is complete here
+          p.counter[q] = 0u;                   // ready for the next call
+          __threadfence_system();
+          asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.ready_out[q] + p.me),
+                       "l"(p.seq)
+                       : "memory");
+        }
+      }
+    }
+    return;
+  }
+  // ---- phase B: this rank's slice, once every producer's partial is in ----
+  if (p.my_slice < 0) return;
+  __shared__ int skip;
+  if (tid == 0) {
+    skip = 0;
+    for (int r = 0; r < 32; ++r) {
+      if (!((p.producers >> r) & 1u)) continue;
+      const unsigned long long t0 = globaltimer();
+      unsigned long long v;
+      for (;;) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.ready_in + r) : "memory");
+        if (v >= p.seq) break;
+        if (*(volatile unsigned int *)p.status & p.guard_mask & (1u << r)) {  // known dead
+          skip = 1;
+          break;
+        }
+        if (globaltimer() - t0 > p.timeout_ns) {
+          atomicOr(p.status, 1u << r);
+          skip = 1;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (skip) return;
+  const int b = blockIdx.x - p.a_ctas;
+  const int nb = gridDim.x - p.a_ctas;
+  const int q = p.my_slice;
+  for (unsigned long long v = p.slice_lo[q] + (unsigned long long)b * FUSED_T + tid;
+       v < p.slice_lo[q + 1]; v += (unsigned long long)nb * FUSED_T) {
+    auto ld = [&](int i) { return ld_cg_f4(p.node[i] + v * 16ull); };
+    float4 r = ProgB::template eval<float4>(p, ld);
+    if (p.divisor != 0.0) r = vdiv(r, p.divisor);
+    for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + v * 16ull, r);
+  }
+  // the bucket's ragged end (n mod 4 elements) belongs to the last slice
+  if (q == p.n_slices - 1 && b == 0 && tid < p.tail) {
+    const unsigned long long e = p.slice_lo[p.n_slices] * 4ull + tid;
+    auto ld = [&](int i) { return __ldcg(reinterpret_cast<const float *>(p.node[i]) + e); };
+    float r = ProgB::template eval<float>(p, ld);
+    if (p.divisor != 0.0) r = __fdiv_rn(r, (float)p.divisor);
+    for (int j = 0; j < p.n_out; ++j) reinterpret_cast<float *>(p.out[j])[e] = r;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1670,6 +1819,7 @@ struct rcv_ctx {
     size_t lo, n;
     int variant;
     unsigned long long call;  // bucket call index that combined it
+    bool fused = false;       // combined by the fused kernel: complete only after a barrier
     // copy-engine all-gather (RCV_CE_GATHER): pull each peer's finished
     // slice of this bucket from its primary into ours before broadcasting
     std::vector<std::pair<const char *, std::pair<size_t, size_t>>> gather;  // src base, [a, z)
@@ -1677,6 +1827,9 @@ struct rcv_ctx {
     int es = 4;
   };
   std::vector<Pending> pending;  // combined buckets awaiting the local broadcast
+  unsigned int *d_counter = nullptr;  // fused kernel: phase-A CTAs done per slice
+  unsigned long long fseq = 0;        // fused kernel: ready-flag sequence
+  bool fused_in_step = false;
   bool timing = false;
   std::vector<TimingRec> recs;
   std::vector<cudaEvent_t> spare_events;
@@ -1705,6 +1858,10 @@ struct rcv_plan {
   int slice_q = 0, slice_nr = 1;
   bool has_bcast = false;
   FoldReq bcast;
+  bool fused = false;                 // one fused kernel per bucket (RCV_FUSED)
+  FusedParams ftmpl;
+  void (*fkern)(FusedParams) = nullptr;
+  int fgrid = 0;
   bool ce_gather = false;             // all-gather by copy engine instead of STG
   std::vector<const char *> peer_primary;  // per live rank (slice order)
   char *my_primary = nullptr;
@@ -1743,6 +1900,9 @@ int ctx_barrier(rcv_ctx *c, uint64_t live, bool participate, cudaStream_t st) {
 // when upto < 0) from this rank's primary replica to its other replicas.
 int ctx_flush(rcv_ctx *c, cudaStream_t st, long long upto) {
   while (!c->pending.empty() && (upto < 0 || (long long)c->pending.front().call <= upto)) {
+    // buckets committed by the fused kernel have no per-bucket barrier: only
+    // the step's closing barrier (upto < 0) proves their slices landed
+    if (upto >= 0 && c->pending.front().fused) break;
     rcv_ctx::Pending e = c->pending.front();
     c->pending.erase(c->pending.begin());
     for (auto &g : e.gather) {
@@ -1792,6 +1952,8 @@ int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer
   CK(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
   for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->ev_arrived[i], cudaEventDisableTiming));
+  CK(cudaMalloc(&c->d_counter, FUSED_MAX_SLICES * sizeof(unsigned int)));
+  CK(cudaMemset(c->d_counter, 0, FUSED_MAX_SLICES * sizeof(unsigned int)));
   *out = c;
   return RCV_OK;
 }
@@ -1807,6 +1969,7 @@ int rcv_ctx_destroy(rcv_ctx *c) {
   cudaEventDestroy(c->ev_main);
   cudaEventDestroy(c->ev_ready);
   for (int i = 0; i < 3; ++i) cudaEventDestroy(c->ev_arrived[i]);
+  cudaFree(c->d_counter);
   cudaStreamDestroy(c->side);
   delete c;
   return RCV_OK;
@@ -1849,6 +2012,7 @@ int rcv_ctx_finish(rcv_ctx *c, uint64_t live_mask, int participate, void *main_s
   rc = ctx_flush(c, st, -1);
   if (rc) return rc;
   c->in_step = false;
+  c->fused_in_step = false;
   return RCV_OK;
 }
 
@@ -1952,6 +2116,87 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
     p->slice_q = d->slice_q;
     p->slice_nr = d->slice_nr;
   }
+  // fused kernel: every local node a full perfect subtree (a forest of at
+  // most 8 roots over fp32 leaves), the combine a tree of at most 64 leaves
+  {
+    // the caller decides from the global cover (every live rank must agree:
+    // the ready flags pair launches across ranks); a rank that cannot
+    // honour it fails loudly rather than desynchronising the sequence
+    bool ok = d->participate && p->has_comb && d->slice_nr <= FUSED_MAX_SLICES &&
+              d->n_pre <= 8 && d->acc_dtype == RCV_F32 &&
+              (p->comb.full_L >= 0 || (p->comb.tree_L >= 0 && p->comb.tree_L <= 6));
+    int total = 0;
+    for (int i = 0; i < d->n_pre && ok; ++i) {
+      ok = d->pre_counts[i] == (int)d->pre_leaves[i];
+      total += d->pre_counts[i];
+    }
+    for (int k = 0; k < total && ok; ++k) ok = d->pre_blocks[k].dtype == RCV_F32;
+    ok = ok && total <= RCV_MAX_IN;
+    if (d->fused && !ok) {
+      delete p;
+      return set_err(RCV_EINVAL, "rcv_plan_create: fused plan requested but this rank's cover is not eligible");
+    }
+    if (d->fused) {
+      FusedParams &f = p->ftmpl;
+      memset(&f, 0, sizeof f);
+      int k = 0;
+      for (int i = 0; i < d->n_pre; ++i) {
+        int L = 0;
+        while ((1 << L) < d->pre_counts[i]) ++L;
+        f.root_L[i] = (uint8_t)L;
+        f.root_first[i] = (uint8_t)k;
+        for (int j = 0; j < d->pre_counts[i]; ++j, ++k) f.leaf[k] = (const char *)d->pre_blocks[k].ptr;
+        f.pool_out[i] = (char *)d->pre_out[i];
+      }
+      f.n_leaf = k;
+      f.n_roots = d->n_pre;
+      f.n_node = p->comb.n_in;
+      for (int i = 0; i < f.n_node; ++i) f.node[i] = p->comb.in[i];
+      memcpy(f.node_in, p->comb.node_in, sizeof f.node_in);
+      memcpy(f.present, p->comb.present, sizeof f.present);
+      f.n_out = p->comb.n_out;
+      for (int j = 0; j < f.n_out; ++j) f.out[j] = p->comb.out[j];
+      f.divisor = d->divisor;
+      f.n_slices = d->slice_nr;
+      f.my_slice = d->slice_q;
+      int q = 0;
+      for (int r = 0; r < 64 && q < d->slice_nr; ++r)
+        if ((d->live_mask >> r) & 1ull) f.ready_out[q++] = ctx->bar.peer[r] + 64;
+      f.ready_in = ctx->bar.local + 64;
+      // wait for every live rank, not only those holding cover nodes: a
+      // rank's ready flag also proves it finished reading this pool set
+      // three calls ago, before phase A overwrites it
+      f.producers = (unsigned int)d->live_mask;
+      f.guard_mask = (unsigned int)d->live_mask;
+      f.me = ctx->me;
+      f.counter = ctx->d_counter;
+      f.status = ctx->bar.status;
+      f.timeout_ns = ctx->bar.timeout_ns;
+      const char *fa = getenv("RCV_FUSED_A");
+      const double frac = fa ? atof(fa) : 0.75;
+      const int L = p->comb.full_L >= 0 ? p->comb.full_L : p->comb.tree_L;
+      const bool full = p->comb.full_L >= 0;
+      void (*tab_full[7])(FusedParams) = {
+          fused_bucket_kernel<ProgFull<0>>, fused_bucket_kernel<ProgFull<1>>,
+          fused_bucket_kernel<ProgFull<2>>, fused_bucket_kernel<ProgFull<3>>,
+          fused_bucket_kernel<ProgFull<4>>, fused_bucket_kernel<ProgFull<5>>,
+          fused_bucket_kernel<ProgFull<6>>};
+      void (*tab_tree[7])(FusedParams) = {
+          fused_bucket_kernel<ProgTree<0>>, fused_bucket_kernel<ProgTree<1>>,
+          fused_bucket_kernel<ProgTree<2>>, fused_bucket_kernel<ProgTree<3>>,
+          fused_bucket_kernel<ProgTree<4>>, fused_bucket_kernel<ProgTree<5>>,
+          fused_bucket_kernel<ProgTree<6>>};
+      p->fkern = full ? tab_full[L] : tab_tree[L];
+      // every CTA co-resident (phase-B CTAs spin on flags phase-A CTAs raise)
+      int occ = 1;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->fkern, FUSED_T, 0));
+      const char *fo = getenv("RCV_FUSED_OCC");
+      if (fo) occ = std::min(occ, std::max(1, atoi(fo)));
+      p->fgrid = ctx->sms * std::max(1, occ);
+      f.a_ctas = std::max(1, std::min(p->fgrid - 1, (int)(frac * p->fgrid)));
+      p->fused = true;
+    }
+  }
   if (d->n_bcast > 0) {
     FoldReq &r = p->bcast;
     r.n_in = 1;
@@ -1981,8 +2226,52 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
   // each kernel's duration is its own (no cross-stream overlap stretching it)
   cudaStream_t side = c->timing ? main : c->side;
   const int es = esize(p->has_comb ? p->comb.acc_dt : RCV_F32);
-  if (!c->in_step) {
-    c->in_step = true;  // leaves were produced on the caller's stream
+  if (p->fused) {
+    // one launch: local partials and this rank's slice of the combine,
+    // synchronised per owner slice by ready flags in peer memory
+    c->in_step = true;
+    c->fused_in_step = true;
+    const unsigned long long j = c->calls++;
+    const size_t set_off = (j % 3) * p->set_stride;
+    FusedParams f = p->ftmpl;
+    uintptr_t mis = 0;
+    for (int i = 0; i < f.n_leaf; ++i) mis |= (uintptr_t)(f.leaf[i] += lo * 4);
+    for (int i = 0; i < f.n_roots; ++i) mis |= (uintptr_t)(f.pool_out[i] += set_off * 4);
+    for (int i = 0; i < f.n_node; ++i) mis |= (uintptr_t)(f.node[i] += set_off * 4);
+    for (int i = 0; i < f.n_out; ++i) mis |= (uintptr_t)(f.out[i] += lo * 4);
+    if (mis & 15)
+      return set_err(RCV_EINVAL, "fused bucket: every leaf, pool slot and output must be 16-byte aligned");
+    const size_t nvec = n / 4, units = (n + 63) / 64;
+    for (int q = 0; q < f.n_slices; ++q) f.slice_lo[q] = std::min(n, units * q / f.n_slices * 64) / 4;
+    f.slice_lo[f.n_slices] = nvec;
+    f.tail = (int)(n % 4);
+    f.seq = ++c->fseq;
+    const double local = (double)(f.n_leaf + f.n_roots) * n * 4;
+    int rc = timed(c, main, 4, local, p->remote_in * (double)n * 4 / f.n_slices,
+                   p->remote_out * (double)n * 4 / f.n_slices, [&]() {
+                     g_launches.fetch_add(1, std::memory_order_relaxed);
+                     p->fkern<<<p->fgrid, FUSED_T, 0, main>>>(f);
+                     CK(cudaGetLastError());
+                     return RCV_OK;
+                   });
+    if (rc) return rc;
+    if (p->has_bcast) {
+      rcv_ctx::Pending e;
+      e.req = p->bcast;
+      e.lo = lo;
+      e.n = n;
+      e.variant = p->variant;
+      e.call = j;
+      e.fused = true;
+      c->pending.push_back(e);
+    }
+    return RCV_OK;
+  }
+  if (!c->in_step || c->fused_in_step) {
+    // leaves were produced on the caller's stream (and, after fused
+    // buckets, the pool sets they used are released only in stream order)
+    c->in_step = true;
+    c->fused_in_step = false;
     CK(cudaEventRecord(c->ev_main, main));
     CK(cudaStreamWaitEvent(c->side, c->ev_main, 0));
   }

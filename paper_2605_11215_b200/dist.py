@@ -35,9 +35,10 @@ barriers and launches.
 
 from __future__ import annotations
 
-from typing import Dict, List, Optional, Sequence
+from typing import Dict, List, Optional, Sequence, Tuple
 
 import ctypes
+import os
 
 import torch
 import torch.distributed as dist
@@ -46,6 +47,35 @@ from . import _lib
 from .comm import Communicator
 from .commit import GradientCommit, aligned_bounds, block_cover
 from .policy import assign_roles, initial_state, policy_advancement
+
+
+# per-rank flag words in peer memory: [0, 64) the step barrier, [64, 128)
+# the fused kernel's per-producer ready sequence
+FLAG_SLOTS = 128
+
+
+def fused_eligible(cover, slot_of, leaves, ranks, b, acc_code, aligned=True) -> bool:
+    """Whether every live rank can run the fused per-bucket kernel on this
+    cover (RCV_FUSED=1 opts in): fp32, at most 8 perfect local nodes and 64
+    local leaves per rank, at most 64 leaves in the combine tree.  Decided
+    from the global cover so all ranks agree."""
+    if os.environ.get("RCV_FUSED", "0") in ("", "0") or acc_code != _lib.F32:
+        return False
+    if b > 64 or len(ranks) > 32 or not aligned:
+        return False
+    if any(t is not None and (t.dtype != torch.float32 or t.data_ptr() % 16)
+           for _, t in leaves.values()):
+        return False
+    per: Dict[int, List[Tuple[int, int]]] = {}
+    for blo, blev in cover:
+        per.setdefault(slot_of[(blo, blev)][0], []).append((blo, blev))
+    for nodes in per.values():
+        if len(nodes) > 8 or sum(1 << lv for _, lv in nodes) > 64:
+            return False
+        for lo, lv in nodes:
+            if sum(1 for m in leaves if lo <= m < lo + (1 << lv)) != 1 << lv:
+                return False
+    return True
 
 
 def owner_slice(n: int, q: int, nr: int, align: int = 64):
@@ -262,13 +292,13 @@ class DistributedGradientCommit(GradientCommit):
             self._shared = vb
             store, store_ptr = vb.share(per * numel * self._es, dtype)
             self.pool, self.pool_ptr = vb.share(3 * pool_slots * self.lmax * self._es, dtype)
-            self.flags, self.flag_ptr = vb.share(64 * 8, torch.int64)
+            self.flags, self.flag_ptr = vb.share(FLAG_SLOTS * 8, torch.int64)
             store.zero_()
             self.flags.zero_()
         else:
             store = torch.zeros(per * numel, dtype=dtype, device=self.device)
             self.pool = torch.empty(3 * pool_slots * self.lmax, dtype=dtype, device=self.device)
-            self.flags = torch.zeros(64, dtype=torch.int64, device=self.device)
+            self.flags = torch.zeros(FLAG_SLOTS, dtype=torch.int64, device=self.device)
             pb = PeerBuffers(self.rank, self.world, group)
             store_ptr = pb.share(store)
             self.pool_ptr = pb.share(self.pool)
@@ -369,7 +399,10 @@ class DistributedGradientCommit(GradientCommit):
             live_mask=mask, participate=int(part),
             remote_in=sum(1 for rk, _ in slot_of.values() if rk != self.rank),
             remote_out=sum(1 for r in prim if not self._holds(r)),
-            guarded=int(self.real_kill))
+            guarded=int(self.real_kill),
+            fused=int(part and fused_eligible(
+                cover, slot_of, leaves, ranks, b, self._code,
+                aligned=self.lmax % 4 == 0 and self.numel % 4 == 0)))
         self.rt.set_plan(d, keep)
 
     def _reduce_bucket(self, k: int, leaves) -> int:

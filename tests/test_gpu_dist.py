@@ -13,16 +13,18 @@ import torch
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 
-def _worker(rank, world, port, combine_variant, q):
+def _worker(rank, world, port, combine_variant, q, fused=False):
     import torch.distributed as dist
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                      RCV_FUSED="1" if fused else "0")
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world,
                             device_id=torch.device("cuda", rank))
     try:
         from paper_2605_11215_b200.dist import DistributedGradientCommit
         from oracle import fold
-        numel = 5 * 64 * 37 + 19
+        # the fused kernel needs 16-byte aligned replica gradients
+        numel = 5 * 64 * 37 + (20 if fused else 19)
         host = [np.random.default_rng(100 + m).standard_normal(numel).astype(np.float32)
                 for m in range(32)]
         dev = [torch.from_numpy(h).cuda() for h in host]
@@ -38,14 +40,19 @@ def _worker(rank, world, port, combine_variant, q):
                 self.plan = [e for e in self.plan if e not in hit]
                 return [r for e in hit for r in e[2]]
 
-        results = []
+        results, kinds = [], set()
         for t, plan in enumerate([[], [("during_sync", 2, [3])], [], [("before_sync", None, [6])]]):
+            if fused:  # (timing serialises the unfused path's two streams)
+                eng.start_timing()
             out = eng.step(t, lambda m, rid: dev[m], Kill(plan))
             torch.cuda.synchronize()
+            if fused:
+                kinds |= {k[0] for k in eng.drain_timing()}
             ok = all(eng.grads[r].cpu().numpy().tobytes() == want.tobytes()
                      for r in eng.comm.members if eng._holds(r))
             results.append((ok, out.contrib_total, sorted(out.contributions.items())))
         eng.check_peers()
+        assert "fused" in kinds or not fused, kinds
         q.put((rank, results))
     except Exception as exc:  # surface the error to the parent
         q.put((rank, repr(exc)))
@@ -53,8 +60,8 @@ def _worker(rank, world, port, combine_variant, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("combine_variant", [0, 2])
-def test_distributed_commit_bitwise(combine_variant):
+@pytest.mark.parametrize("combine_variant,fused", [(0, False), (2, False), (0, True)])
+def test_distributed_commit_bitwise(combine_variant, fused):
     world = min(torch.cuda.device_count(), 4)
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -62,7 +69,7 @@ def test_distributed_commit_bitwise(combine_variant):
     s.close()
     ctx = torch.multiprocessing.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, combine_variant, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, combine_variant, q, fused))
              for r in range(world)]
     for p in procs:
         p.start()
