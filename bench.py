@@ -380,8 +380,11 @@ def run_ours(args):
             "nvlink_gbs_per_direction": (k["nvl_in"] + k["nvl_out"]) / sec / 1e9 if sec else None}
     dom = max(kinds, key=lambda kk: kinds[kk]["ms"]) if kinds else None
     fail_idx = [i for i, o in enumerate(outcomes) if o.events]
-    normal = [ms for i, ms in enumerate(step_ms) if i not in fail_idx]
-    recovery_ms = (step_ms[fail_idx[0]] - statistics.median(normal)) if fail_idx and normal else None
+    # recovery: the failure step against the failure-free steps before it
+    # (the steps after it run the degraded layout, reported separately)
+    pre = step_ms[:fail_idx[0]] if fail_idx else step_ms
+    post = step_ms[fail_idx[-1] + 1:] if fail_idx else []
+    recovery_ms = (step_ms[fail_idx[0]] - statistics.median(pre)) if fail_idx and pre else None
 
     # correctness spot check inside the bench: every live replica holds the
     # same bytes (one kernel wrote them all)
@@ -417,6 +420,8 @@ def run_ours(args):
         "recovery_ms": recovery_ms,
         "step_ms": {"median": statistics.median(step_ms), "max": max(step_ms),
                     "failure_step": step_ms[fail_idx[0]] if fail_idx else None,
+                    "failure_free_median": statistics.median(pre) if pre else None,
+                    "degraded_median": statistics.median(post) if post else None,
                     "all": [round(x, 3) for x in step_ms]},
         "replica_agreement": agree,
         "host_enqueue_ms_per_step": host_ms,

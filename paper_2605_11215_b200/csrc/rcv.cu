@@ -720,6 +720,7 @@ struct BarrierParams {
   unsigned long long timeout_ns;
   int n;
   int me;
+  int fence;  // leading __threadfence_system (RCV_BAR_FENCE, default on)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -735,7 +736,7 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   const bool peer = t < p.n && t != p.me && ((p.live >> t) & 1ull) && !((dead >> t) & 1u);
   // everything this GPU wrote before this kernel (partials, remote stores)
   // is made visible system-wide before the flag store releases it
-  __threadfence_system();
+  if (p.fence) __threadfence_system();
   if (peer)
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.peer[t] + p.me), "l"(p.value)
                  : "memory");
@@ -1711,6 +1712,7 @@ int rcv_barrier(uint64_t *local_flags, void *const *peer_flags, int n, int me,
   p.timeout_ns = timeout_ns;
   p.n = n;
   p.me = me;
+  p.fence = 1;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
   CK(cudaGetLastError());
@@ -1941,6 +1943,10 @@ int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer
   c->bar.timeout_ns = timeout_ns;
   c->bar.n = n_ranks;
   c->bar.me = me;
+  {
+    const char *bf = getenv("RCV_BAR_FENCE");
+    c->bar.fence = bf ? atoi(bf) : 1;
+  }
   // the side stream carries the HBM-bound critical path (pre-reduce and
   // local broadcast); RCV_SIDE_PRIORITY=1 schedules its CTAs ahead of the
   // NVLink-bound combine on the caller's stream
@@ -2024,12 +2030,21 @@ static int env_ctas(const char *name, int sms, double dflt_frac) {
   return std::max(1, (int)(f * sms));      // a fraction of the SMs
 }
 
+// SM shares of the two concurrent streams (profiles/r1/caps_sweep.txt): the
+// NVLink-bound combine saturates the links with about a third of the SMs,
+// and a full-occupancy grid of either kernel would keep the other off the
+// GPU until its last wave drains.  Measured at N=4 on configs[1]: 2.95 ->
+// 2.60 ms/step (failure-free 2.27 -> 1.91, degraded 3.59 -> 3.28); N=2
+// neutral.  RCV_COMB_CTAS / RCV_PRE_CTAS override (0: uncapped).
+constexpr double kCombShare = 0.35, kPreShare = 0.65;
+
 int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
   rcv_plan *p = new rcv_plan();
   p->ctx = ctx;
   p->set_stride = d->set_stride;
   p->variant = d->variant;
   p->comb_variant = d->comb_variant;
+  if (const char *cv = getenv("RCV_COMB_VARIANT")) p->comb_variant = atoi(cv);  // experiments
   p->live_mask = d->live_mask;
   p->participate = d->participate != 0;
   p->remote_in = d->remote_in;
@@ -2044,7 +2059,7 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       delete p;
       return rc;
     }
-    r.max_ctas = env_ctas("RCV_PRE_CTAS", ctx->sms, 0.0);
+    r.max_ctas = env_ctas("RCV_PRE_CTAS", ctx->sms, kPreShare);
     p->pre.push_back(r);
     p->pre_count.push_back(d->pre_counts[i]);
     off += d->pre_counts[i];
@@ -2084,7 +2099,7 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       r.n_out = d->n_pre;
       r.n_roots = d->n_pre;
       r.acc_dt = d->acc_dtype;
-      r.max_ctas = env_ctas("RCV_PRE_CTAS", ctx->sms, 0.0);
+      r.max_ctas = env_ctas("RCV_PRE_CTAS", ctx->sms, kPreShare);
       p->has_forest = true;
       p->forest_count = k;
     }
@@ -2106,7 +2121,7 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       delete p;
       return rc;
     }
-    p->comb.max_ctas = env_ctas("RCV_COMB_CTAS", ctx->sms, 0.0);
+    p->comb.max_ctas = env_ctas("RCV_COMB_CTAS", ctx->sms, kCombShare);
     if (d->guarded) {
       // the combine reads live peers' partials: skip it once one timed out
       p->comb.guard = (const unsigned int *)ctx->bar.status;
