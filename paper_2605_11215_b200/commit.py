@@ -7,8 +7,9 @@ order, whatever the failures.  Compared with the drop-in ``run_iteration``
 changes only the data plane:
 
 * **Canonical addressing.**  Step microbatch indices 0..B-1 are handed out
-  in contiguous ranges, ascending replica id, by the quota policy (majors G,
-  the minor R; ``policy.py``).  A spare shadows a counterpart (major-spares
+  by the quota policy (majors G, the minor R; ``policy.py``): in contiguous
+  ranges, ascending replica id (``_canonical_ranges``; the multi-process
+  engine packs each rank's share into aligned dyadic blocks instead).  A spare shadows a counterpart (major-spares
   the highest-id majors, the minor-spare the minor); on promotion it admits
   the vacated replica's range.  In a boundary extension the survivors take
   the orphaned indices (those no live replica admitted), smallest first.
@@ -155,6 +156,18 @@ class GradientCommit:
         single-process mode; the distributed engine overrides)."""
         return True
 
+    def _canonical_ranges(self, counts: List[Tuple[int, int]]) -> Dict[int, List[int]]:
+        """Canonical microbatch indices of each replica, given its quota
+        (members in ascending id order): contiguous ranges, ascending id.
+        Any partition of [0, sum) commits the same bits; subclasses pick one
+        that suits their data placement."""
+        ranges: Dict[int, List[int]] = {}
+        pos = 0
+        for rid, q in counts:
+            ranges[rid] = list(range(pos, pos + q))
+            pos += q
+        return ranges
+
     def _end_of_step(self) -> None:
         """Hook run after the last bucket of a step is committed."""
 
@@ -290,14 +303,12 @@ class GradientCommit:
         comm.reset_iteration()
 
         # canonical ranges (contributor quota) and spare shadows
-        ranges: Dict[int, List[int]] = {}
-        pos = 0
+        counts = []
         for rid in comm.members:
             role = comm.roles[rid]
-            q = state.g_cur if role is ReplicaRole.MAJOR else (
-                state.r_cur if role is ReplicaRole.MINOR else 0)
-            ranges[rid] = list(range(pos, pos + q))
-            pos += q
+            counts.append((rid, state.g_cur if role is ReplicaRole.MAJOR else (
+                state.r_cur if role is ReplicaRole.MINOR else 0)))
+        ranges = self._canonical_ranges(counts)
         majors = [r for r in comm.members if comm.roles[r] is ReplicaRole.MAJOR]
         minors = [r for r in comm.members if comm.roles[r] is ReplicaRole.MINOR]
         shadow: Dict[int, int] = {}

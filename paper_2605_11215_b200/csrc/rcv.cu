@@ -1858,6 +1858,8 @@ struct rcv_plan {
   bool has_comb = false;
   FoldReq comb;
   int slice_q = 0, slice_nr = 1;
+  // first element of owner slice q of a bucket of `units` 64-element units
+  size_t slice_at(size_t units, int q) const { return units * q / slice_nr * 64; }
   bool has_bcast = false;
   FoldReq bcast;
   bool fused = false;                 // one fused kernel per bucket (RCV_FUSED)
@@ -2257,7 +2259,7 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
     if (mis & 15)
       return set_err(RCV_EINVAL, "fused bucket: every leaf, pool slot and output must be 16-byte aligned");
     const size_t nvec = n / 4, units = (n + 63) / 64;
-    for (int q = 0; q < f.n_slices; ++q) f.slice_lo[q] = std::min(n, units * q / f.n_slices * 64) / 4;
+    for (int q = 0; q < f.n_slices; ++q) f.slice_lo[q] = std::min(n, p->slice_at(units, q)) / 4;
     f.slice_lo[f.n_slices] = nvec;
     f.tail = (int)(n % 4);
     f.seq = ++c->fseq;
@@ -2329,8 +2331,8 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
   CK(cudaEventRecord(c->ev_arrived[j % 3], main));
   if (p->has_comb) {
     const size_t units = (n + 63) / 64;
-    const size_t a = std::min(n, units * p->slice_q / p->slice_nr * 64);
-    const size_t z = std::min(n, units * (p->slice_q + 1) / p->slice_nr * 64);
+    const size_t a = std::min(n, p->slice_at(units, p->slice_q));
+    const size_t z = std::min(n, p->slice_at(units, p->slice_q + 1));
     if (z > a) {
       FoldReq r = p->comb;
       shift(r, set_off + a, lo + a);
@@ -2353,8 +2355,8 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
     const size_t units = (n + 63) / 64;
     for (int q = 0; q < p->slice_nr; ++q) {
       if (q == p->slice_q) continue;
-      const size_t a = std::min(n, units * q / p->slice_nr * 64);
-      const size_t z = std::min(n, units * (q + 1) / p->slice_nr * 64);
+      const size_t a = std::min(n, p->slice_at(units, q));
+      const size_t z = std::min(n, p->slice_at(units, q + 1));
       e.gather.push_back({p->peer_primary[q], {a, z}});
     }
     c->pending.push_back(e);

@@ -80,7 +80,10 @@ def fused_eligible(cover, slot_of, leaves, ranks, b, acc_code, aligned=True) -> 
 
 def owner_slice(n: int, q: int, nr: int, align: int = 64):
     """[a, z) of a bucket of n elements owned by the q-th of nr live ranks:
-    contiguous, align-element granular, covering [0, n) exactly."""
+    contiguous, align-element granular, covering [0, n) exactly.  Equal
+    slices: every owner reads every cover node's partial, so the combine's
+    work per element is the same on every owner (NVLink-direction-balanced
+    unequal slices measured slower: profiles/r1/slice_weights.txt)."""
     units = (n + align - 1) // align
     return (min(n, units * q // nr * align), min(n, units * (q + 1) // nr * align))
 
@@ -316,6 +319,56 @@ class DistributedGradientCommit(GradientCommit):
 
     def _holds(self, rid: int) -> bool:
         return self.rank_of[rid] == self.rank
+
+    def _canonical_ranges(self, counts: List[Tuple[int, int]]) -> Dict[int, List[int]]:
+        """Pack each rank's microbatch count into aligned dyadic blocks.
+
+        A rank's leaves enter the commit as the maximal aligned tree nodes
+        it owns whole (block_cover), and every owner slice of the combine
+        reads every node's partial, so the combine's NVLink bytes grow with
+        the cover size.  Contiguous ranges fragment once per-rank counts stop
+        being powers of two (10/5/10/7 after a death at N=4: 11 nodes).
+        Decomposing each count into its binary digits and placing the blocks
+        largest first (buddy order: every start is a multiple of the block
+        size, and the packing stays within [0, sum)) reaches sum of
+        popcounts (9 there).  Absent leaves past the sum and the per-node
+        leaf cap can favour the contiguous layout for large counts, so the
+        smaller cover of the two is kept.  The committed bits do not change:
+        the canonical tree depends only on the leaf values."""
+        key = tuple(counts)
+        memo = self.__dict__.setdefault("_ranges_memo", {})
+        if key not in memo:
+            packed = self._dyadic_ranges(counts)
+            plain = GradientCommit._canonical_ranges(self, counts)
+            total = sum(q for _, q in counts)
+
+            def nodes(ranges):
+                owner = {i: self.rank_of[r] for r, ids in ranges.items() for i in ids}
+                return len(block_cover(owner, max(1, total))) if owner else 0
+            memo[key] = packed if nodes(packed) < nodes(plain) else plain
+        return {r: list(v) for r, v in memo[key].items()}
+
+    def _dyadic_ranges(self, counts: List[Tuple[int, int]]) -> Dict[int, List[int]]:
+        per_rank: Dict[int, List[Tuple[int, int]]] = {}
+        for rid, q in counts:
+            per_rank.setdefault(self.rank_of[rid], []).append((rid, q))
+        blocks = []
+        for rk, lst in per_rank.items():
+            c = sum(q for _, q in lst)
+            blocks += [(1 << bit, rk) for bit in range(c.bit_length()) if (c >> bit) & 1]
+        blocks.sort(key=lambda x: (-x[0], x[1]))
+        ids: Dict[int, List[int]] = {rk: [] for rk in per_rank}
+        pos = 0
+        for size, rk in blocks:
+            ids[rk].extend(range(pos, pos + size))
+            pos += size
+        ranges: Dict[int, List[int]] = {}
+        for rk, lst in per_rank.items():
+            k = 0
+            for rid, q in lst:
+                ranges[rid] = ids[rk][k:k + q]
+                k += q
+        return ranges
 
     def _live_ranks(self) -> List[int]:
         return sorted({self.rank_of[r] for r in self.comm.members})

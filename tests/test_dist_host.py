@@ -9,7 +9,8 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2605_11215_b200.dist import owner_slice, plan_bucket
+from paper_2605_11215_b200.commit import block_cover
+from paper_2605_11215_b200.dist import DistributedGradientCommit, owner_slice, plan_bucket
 
 
 def test_owner_slices_partition():
@@ -80,3 +81,60 @@ def test_replicated_plan_agrees_world2():
     assert a[:4] == b[:4]                 # same decision and plan on both ranks
     assert a[0] == 28 and a[1] is True    # census of 7 survivors x 4
     assert a[4][1] == b[4][0] and a[4][0] == 0 and b[4][1] == 6221990
+
+
+def test_dyadic_packing_minimises_cover():
+    """_canonical_ranges packs each rank's count into aligned blocks: a
+    partition of [0, sum) whose cover has sum-of-popcounts nodes (the
+    minimum), e.g. 9 instead of 11 for the N=4 layout after replica 3 dies."""
+    import random
+    class Fake:
+        _dyadic_ranges = DistributedGradientCommit._dyadic_ranges
+        _canonical_ranges = DistributedGradientCommit._canonical_ranges
+
+    def pack(f, counts):
+        f.__dict__.pop("_ranges_memo", None)
+        return f._canonical_ranges(counts)
+
+    def cover_size(ranges, rank_of, b):
+        owner = {i: rank_of[r] for r, ids in ranges.items() for i in ids}
+        return len(block_cover(owner, b))
+
+    f = Fake()
+    f.rank_of = {r: r // 2 for r in range(8)}
+    assert len(pack(f, [(0, 8), (1, 8)])[1]) == 8
+    counts = [(0, 5), (1, 5), (2, 5), (4, 5), (5, 5), (6, 5), (7, 2)]
+    got = pack(f, counts)
+    contiguous, pos = {}, 0
+    for r, q in counts:
+        contiguous[r] = list(range(pos, pos + q))
+        pos += q
+    assert cover_size(contiguous, f.rank_of, 32) == 11
+    assert cover_size(got, f.rank_of, 32) == 9
+    rng = random.Random(3)
+    for _ in range(300):
+        world = rng.choice([2, 3, 4, 8])
+        per = rng.choice([1, 2, 4])
+        f.rank_of = {r: r // per for r in range(world * per)}
+        counts = [(r, rng.randint(0, 9)) for r in range(world * per)]
+        total = sum(q for _, q in counts)
+        got = pack(f, counts)
+        ids = sorted(i for v in got.values() for i in v)
+        assert ids == list(range(total))
+        assert all(len(got[r]) == q for r, q in counts)
+        by_rank = {}
+        for r, q in counts:
+            by_rank[f.rank_of[r]] = by_rank.get(f.rank_of[r], 0) + q
+        if total:
+            # (absent leaves past `total` can merge a rank's last block
+            # upward, so the popcount sum is an upper bound here)
+            want = sum(bin(c).count("1") for c in by_rank.values())
+            contiguous, pos = {}, 0
+            for r, q in counts:
+                contiguous[r] = list(range(pos, pos + q))
+                pos += q
+            got_n = cover_size(got, f.rank_of, total)
+            assert got_n <= cover_size(contiguous, f.rank_of, total)
+            if total <= 64:
+                assert got_n <= want
+
