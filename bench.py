@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=1 << 23)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--trace", default="", help="torch.profiler chrome trace prefix (diagnostics)")
+    ap.add_argument("--trace-degraded", action="store_true",
+                    help="with --trace: kill the victim in warmup step 0, trace the degraded layout")
     return ap.parse_args()
 
 
@@ -281,6 +283,8 @@ def run_ours(args):
               for _ in range(M)]
     total_steps = args.warmup + args.steps
     fail_step = -1 if args.no_fail else args.warmup + args.steps // 2
+    if args.trace and args.trace_degraded:
+        fail_step = 0
     if world > 1:
         from paper_2605_11215_b200.dist import DistributedGradientCommit
         eng = DistributedGradientCommit(numel, W, G, args.buckets, variant=args.variant,
@@ -356,28 +360,21 @@ def run_ours(args):
     tokens = committed * TOKENS_PER_MB
     value = tokens / (elapsed_ms / 1e3)
 
-    # roofline per kernel kind over the timed region (CUDA events on the
-    # launching stream around every launch)
-    kinds = {}
-    for kind, ms, nb, nin, nout in recs:
-        k = kinds.setdefault(kind, {"launches": 0, "ms": 0.0, "bytes": 0, "nvl_in": 0, "nvl_out": 0})
-        k["launches"] += 1
-        k["ms"] += ms
-        k["bytes"] += nb
-        k["nvl_in"] += nin
-        k["nvl_out"] += nout
+    # the same per-kernel pass over 2 steps of the degraded layout (after the
+    # timed region, so the headline is unperturbed)
+    recs_deg = []
+    if fail_step >= 0:
+        eng.start_timing()
+        for s in range(2):
+            eng.step(total_steps + s, leaf, None)
+        torch.cuda.synchronize()
+        recs_deg = eng.drain_timing()
+        if world > 1:
+            torch.distributed.barrier()
+
+    kinds, per_kind = summarise_kernels(recs)
+    per_kind_deg = summarise_kernels(recs_deg)[1]
     peak, peak_kind = peaks()
-    per_kind = {}
-    for kind, k in kinds.items():
-        sec = k["ms"] / 1e3
-        # NVLink per direction: this rank's remote reads arrive inbound while
-        # the peers' reads of its slices leave outbound (and its remote
-        # stores leave while the peers' arrive), so with symmetric traffic
-        # each direction carries remote reads + remote writes
-        per_kind[kind] = {
-            "launches": k["launches"], "mean_launch_us": 1e3 * k["ms"] / k["launches"],
-            "hbm_gbs": k["bytes"] / sec / 1e9 if sec else None,
-            "nvlink_gbs_per_direction": (k["nvl_in"] + k["nvl_out"]) / sec / 1e9 if sec else None}
     dom = max(kinds, key=lambda kk: kinds[kk]["ms"]) if kinds else None
     fail_idx = [i for i, o in enumerate(outcomes) if o.events]
     # recovery: the failure step against the failure-free steps before it
@@ -414,6 +411,7 @@ def run_ours(args):
                    "parallelism": "dp8-sim"},
         "roofline": roofline(dom, per_kind, peak, peak_kind),
         "kernels": per_kind,
+        "kernels_degraded": per_kind_deg or None,
         # masked-allreduce algorithmic bandwidth: gradient bytes committed
         # (reduced over the live replicas and scaled) per second of step time
         "allreduce_algbw_gbs": numel * 4 / (elapsed_ms / args.steps / 1e3) / 1e9,
@@ -445,6 +443,31 @@ NVLINK_PEAK = 770.0  # GB/s per direction, measured peer copy (B200_PROFILING.md
 # dram read+write bytes per launch of the dominant kernel, ncu --set full
 # (profiles/r1/ncu_full_fold_direct_ProgFull5.txt: 796.4 MB + 147.9 MB)
 TRAFFIC = {"fused": 944.3e6}
+
+
+def summarise_kernels(recs):
+    """Per kernel kind: launches, mean launch time, HBM and NVLink rates
+    (CUDA events on the launching stream around every launch)."""
+    kinds = {}
+    for kind, ms, nb, nin, nout in recs:
+        k = kinds.setdefault(kind, {"launches": 0, "ms": 0.0, "bytes": 0, "nvl_in": 0, "nvl_out": 0})
+        k["launches"] += 1
+        k["ms"] += ms
+        k["bytes"] += nb
+        k["nvl_in"] += nin
+        k["nvl_out"] += nout
+    per_kind = {}
+    for kind, k in kinds.items():
+        sec = k["ms"] / 1e3
+        # NVLink per direction: this rank's remote reads arrive inbound while
+        # the peers' reads of its slices leave outbound (and its remote
+        # stores leave while the peers' arrive), so with symmetric traffic
+        # each direction carries remote reads + remote writes
+        per_kind[kind] = {
+            "launches": k["launches"], "mean_launch_us": 1e3 * k["ms"] / k["launches"],
+            "hbm_gbs": k["bytes"] / sec / 1e9 if sec else None,
+            "nvlink_gbs_per_direction": (k["nvl_in"] + k["nvl_out"]) / sec / 1e9 if sec else None}
+    return kinds, per_kind
 
 
 def roofline(dom, per_kind, peak, peak_kind):

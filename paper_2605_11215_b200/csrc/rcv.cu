@@ -1136,7 +1136,8 @@ int launch_vec(const FoldReq &r, bool tma, const TmaGeom &g, int maxd,
       default: RCV_LAUNCH(ProgFull<6>);
     }
   }
-  if (r.tree_L >= 0 && r.tree_L <= 6) {
+  static const bool tree_as_stack = getenv("RCV_TREE_EVAL") && atoi(getenv("RCV_TREE_EVAL")) == 1;
+  if (r.tree_L >= 0 && r.tree_L <= 6 && !(tree_as_stack && maxd <= 8)) {
     switch (r.tree_L) {
       case 0: RCV_LAUNCH(ProgTree<0>);
       case 1: RCV_LAUNCH(ProgTree<1>);
@@ -1171,7 +1172,8 @@ int common_head(const FoldReq &r) {
 int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int sms) {
   if (numel == 0 || r.n_out == 0) return RCV_OK;
   int maxd = 1;
-  int rc = program_depth(r.op, r.n_in, &maxd);
+  // a forest's inputs are its roots' leaves, not a stack program
+  int rc = r.n_roots > 0 ? RCV_OK : program_depth(r.op, r.n_in, &maxd);
   if (rc) return rc;
   if (r.n_in == 0) {
     for (int j = 0; j < r.n_out; ++j) CK(cudaMemsetAsync(r.out[j], 0, numel * esize(r.acc_dt), st));
@@ -2106,6 +2108,12 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       p->forest_count = k;
     }
   }
+  if (getenv("RCV_DEBUG")) {
+    fprintf(stderr, "[rcv] rank %d plan: n_pre %d forest %d counts", ctx->me, d->n_pre, (int)p->has_forest);
+    for (int i = 0; i < d->n_pre; ++i) fprintf(stderr, " %d/%u", d->pre_counts[i], d->pre_leaves[i]);
+    fprintf(stderr, " | n_comb %d tree_L %d full_L %d\n", d->n_comb, p->has_comb ? p->comb.tree_L : -9,
+            p->has_comb ? p->comb.full_L : -9);
+  }
   p->ce_gather = getenv("RCV_CE_GATHER") && atoi(getenv("RCV_CE_GATHER")) && d->participate &&
                  d->n_comb_out > 1;
   if (p->ce_gather) {
@@ -2311,10 +2319,15 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
   if (p->has_forest && n % 64 == 0) {
     FoldReq r = p->forest;
     shift(r, lo, set_off);
-    const double bytes = (double)(p->forest_count + r.n_out) * n * esize(r.acc_dt);
-    int rc = timed(c, side, 0, bytes, 0, 0,
-                   [&]() { return run_fold(r, n, p->variant, side, c->sms); });
-    forest_done = rc == RCV_OK;  // misaligned leaves: fall back to per-node launches
+    // the forest evaluator needs 16-byte aligned whole vectors; misaligned
+    // leaves (a caller's odd tensor offsets) take the per-node launches
+    if (common_head(r) == 0) {
+      const double bytes = (double)(p->forest_count + r.n_out) * n * esize(r.acc_dt);
+      int rc = timed(c, side, 0, bytes, 0, 0,
+                     [&]() { return run_fold(r, n, p->variant, side, c->sms); });
+      if (rc) return rc;
+      forest_done = true;
+    }
   }
   for (size_t i = 0; i < p->pre.size() && !forest_done; ++i) {
     FoldReq r = p->pre[i];

@@ -9,5 +9,7 @@ for E in "$@"; do
   python3 -c "
 import json; ls=[l for l in open('gpurun_out/envab_$i.json') if l.startswith('{')]
 d=json.loads(ls[-1]); a=d['step_ms']['all']; k=d['kernels']
-print('N$N [$E]', round(d['ms_per_step'],3), 'free', a[3], 'fail', round(d['step_ms']['failure_step'],2), 'post', a[-1], {n:(round(v['mean_launch_us']),round(v['nvlink_gbs_per_direction'] or 0)) for n,v in k.items()})" || echo "N$N [$E] failed"
+kd=d.get('kernels_degraded') or {}
+f=lambda k: {n:(round(v['mean_launch_us']),round(v['nvlink_gbs_per_direction'] or 0)) for n,v in k.items()}
+print('N$N [$E]', round(d['ms_per_step'],3), 'free', a[3], 'fail', round(d['step_ms']['failure_step'],2), 'post', a[-1], f(k), 'degraded', f(kd))" || echo "N$N [$E] failed"
 done
