@@ -265,7 +265,86 @@ struct FoldParams {
   // canonical tree (ProgTree): heap-indexed nodes, id = 2^(L-level)-1+idx
   int8_t node_in[2 * RCV_MAX_IN - 1];    // input feeding the node, or -1
   uint8_t present[2 * RCV_MAX_IN - 1];   // subtree holds at least one input
+  // flag gate (multi-process runtime, gate_mask != 0): before its first read
+  // every CTA waits until gate_flags[r] >= gate_value for each rank bit r
+  // (the producers' "partials ready" sequence, raised from peer GPUs), and
+  // the last CTA to finish releases done_value into every done_out[i] (the
+  // consumers' "this call's pool set is read and its slices are stored")
+  const unsigned long long *gate_flags;
+  unsigned long long gate_value;
+  unsigned int gate_mask;
+  unsigned int *gate_status;  // timeout / dead-peer bits (barrier status word)
+  unsigned long long gate_timeout_ns;
+  unsigned int *done_counter;  // device-local CTA count, reset by the last CTA
+  unsigned long long *done_out[32];
+  int n_done;
+  unsigned long long done_value;
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// One thread waits until flags[r] >= value for every rank bit r of mask,
+// each wait bounded by %globaltimer.  A rank already marked in *status, or
+// one that times out (then marked), is not waited for; with `strict` the
+// call then returns false (the caller must not read that rank's memory).
+__device__ __noinline__ bool flag_wait(const unsigned long long *flags, unsigned long long value,
+                                       unsigned int mask, unsigned int *status,
+                                       unsigned long long timeout_ns, bool strict) {
+  bool ok = true;
+  for (int r = 0; r < 32; ++r) {
+    if (!((mask >> r) & 1u)) continue;
+    const unsigned long long t0 = globaltimer();
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + r) : "memory");
+      if (v >= value) break;
+      if (*(volatile unsigned int *)status & (1u << r)) {  // known dead
+        ok = !strict && ok;
+        break;
+      }
+      if (globaltimer() - t0 > timeout_ns) {
+        atomicOr(status, 1u << r);
+        ok = !strict && ok;
+        break;
+      }
+    }
+  }
+  return ok;
+}
+
+// Every thread of the CTA calls this before its first load of a gated launch:
+// thread 0 acquires the producers' ready flags; false when one of them is
+// dead or timed out (then nothing may be read, but gate_done still runs).
+__device__ __noinline__ bool gate_enter(const FoldParams &p) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0)
+    s_ok = !(p.guard && (*p.guard & p.guard_mask)) &&
+           flag_wait(p.gate_flags, p.gate_value, p.gate_mask, p.gate_status, p.gate_timeout_ns, true);
+  __syncthreads();
+  return s_ok != 0;
+}
+
+// Every thread of the CTA calls this after its last store of a gated launch:
+// the CTA's stores are made visible system-wide, counted, and the last CTA of
+// the grid releases the done sequence to every consumer rank.
+__device__ __noinline__ void gate_done(const FoldParams &p) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(p.done_counter, 1u);
+    if (prev + 1 == gridDim.x) {
+      atomicExch(p.done_counter, 0u);  // ready for the next gated launch
+      __threadfence_system();
+      for (int i = 0; i < p.n_done; ++i)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.done_out[i]), "l"(p.done_value)
+                     : "memory");
+    }
+  }
+}
 
 // ---------------------------------------------------------------------------
 // fold programs: evaluate one accumulator-vector from a loader ld(i) -> V.
@@ -395,11 +474,20 @@ __device__ __forceinline__ void emit(const FoldParams &p, const Ld &ld, unsigned
 // ---------------------------------------------------------------------------
 // DIRECT variant: 128-bit LDG straight from (local or peer) global memory
 
-template <typename A, typename Prog>
+template <typename A, typename Prog, bool kGate = false>
 __global__ void __launch_bounds__(256)
     fold_direct_kernel(const __grid_constant__ FoldParams p) {
   using V = typename VecT<A>::V;
-  if (p.guard && (*p.guard & p.guard_mask)) return;
+  if constexpr (kGate) {
+    // the loads below are L1::no_allocate, so no line of a pool slot can be
+    // cached on this SM before its producer's ready flag was acquired
+    if (!gate_enter(p)) {
+      gate_done(p);
+      return;
+    }
+  } else if (p.guard && (*p.guard & p.guard_mask)) {
+    return;
+  }
   for (unsigned long long v = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
        v < p.nvec; v += (unsigned long long)gridDim.x * blockDim.x) {
     auto ld = [&](int i) {
@@ -408,6 +496,7 @@ __global__ void __launch_bounds__(256)
     };
     emit<Prog, V>(p, ld, v * (unsigned long long)VecT<A>::OUT);
   }
+  if constexpr (kGate) gate_done(p);
 }
 
 // ---------------------------------------------------------------------------
@@ -455,16 +544,18 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src,
       : "memory");
 }
 
-template <typename A, typename Prog>
+template <typename A, typename Prog, bool kGate = false>
 __global__ void __launch_bounds__(TMA_THREADS)
     fold_tma_kernel(const __grid_constant__ FoldParams p) {
   using V = typename VecT<A>::V;
-  if (p.guard && (*p.guard & p.guard_mask)) return;  // uniform: before any barrier
+  const bool guarded = p.guard && (*p.guard & p.guard_mask);
+  if (!kGate && guarded) return;  // uniform: before any barrier
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)p.stages * p.stage_bytes);
   uint64_t *empty = full + p.stages;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  __shared__ int s_skip;
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
@@ -472,11 +563,20 @@ __global__ void __launch_bounds__(TMA_THREADS)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // gated launch: this thread is also the TMA producer, so its acquire of
+    // the producers' ready flags, followed by a generic->async proxy fence,
+    // orders every bulk copy below after the peers' partial stores
+    s_skip = 0;
+    if constexpr (kGate) {
+      s_skip = guarded || !flag_wait(p.gate_flags, p.gate_value, p.gate_mask, p.gate_status,
+                                     p.gate_timeout_ns, true);
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
   }
   __syncthreads();
 
   const unsigned long long tv = (unsigned long long)TMA_CONSUMERS * p.vpt;
-  const unsigned long long ntiles = (p.nvec + tv - 1) / tv;
+  const unsigned long long ntiles = s_skip ? 0 : (p.nvec + tv - 1) / tv;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -501,6 +601,7 @@ __global__ void __launch_bounds__(TMA_THREADS)
         }
       }
     }
+    if constexpr (kGate) gate_done(p);
     return;
   }
 
@@ -528,6 +629,7 @@ __global__ void __launch_bounds__(TMA_THREADS)
       phase ^= 1;
     }
   }
+  if constexpr (kGate) gate_done(p);
 }
 
 // ---------------------------------------------------------------------------
@@ -723,12 +825,6 @@ struct BarrierParams {
   int fence;  // leading __threadfence_system (RCV_BAR_FENCE, default on)
 };
 
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
 __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   const int t = threadIdx.x;
   // a peer that already timed out is dead: never signal or wait on it again
@@ -754,6 +850,35 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   }
   __syncthreads();
   __threadfence_system();
+}
+
+// Flag signal / wait of the gated runtime (RCV_GATE): release `signal_value`
+// into every signal[i] after a system fence (so everything this GPU wrote
+// before the launch is visible to the peers that acquire it), then wait until
+// wait_flags[r] >= wait_value for each rank bit of wait_mask.  Dead or
+// timed-out ranks are skipped and marked in the status word.
+struct GateParams {
+  unsigned long long *signal[32];
+  int n_signal;
+  unsigned long long signal_value;
+  const unsigned long long *wait_flags;
+  unsigned long long wait_value;
+  unsigned int wait_mask;
+  unsigned int *status;
+  unsigned long long timeout_ns;
+};
+
+__global__ void gate_kernel(const __grid_constant__ GateParams p) {
+  const int t = threadIdx.x;
+  if (p.n_signal) {
+    __threadfence_system();
+    if (t < p.n_signal)
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.signal[t]), "l"(p.signal_value)
+                   : "memory");
+  }
+  if (p.wait_mask && t == 0)
+    flag_wait(p.wait_flags, p.wait_value, p.wait_mask, p.status, p.timeout_ns, false);
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
@@ -947,6 +1072,16 @@ struct FoldReq {
   uint8_t root_first[8] = {};
   int8_t node_in[2 * RCV_MAX_IN - 1];
   uint8_t present[2 * RCV_MAX_IN - 1];
+  // flag gate of a single vector launch (FoldParams::gate_*), runtime only
+  const unsigned long long *gate_flags = nullptr;
+  unsigned long long gate_value = 0;
+  unsigned int gate_mask = 0;
+  unsigned int *gate_status = nullptr;
+  unsigned long long gate_timeout_ns = 0;
+  unsigned int *done_counter = nullptr;
+  unsigned long long *done_out[32];
+  int n_done = 0;
+  unsigned long long done_value = 0;
 };
 
 enum { PK_STACK = 0, PK_LEFT = 1, PK_TREE = 2 };
@@ -1025,6 +1160,15 @@ void fill_vec_params(FoldParams &p, const FoldReq &r, unsigned long long e0,
   p.guard = r.guard;
   p.guard_mask = r.guard_mask;
   p.n_roots = r.n_roots;
+  p.gate_flags = r.gate_flags;
+  p.gate_value = r.gate_value;
+  p.gate_mask = r.gate_mask;
+  p.gate_status = r.gate_status;
+  p.gate_timeout_ns = r.gate_timeout_ns;
+  p.done_counter = r.done_counter;
+  for (int i = 0; i < r.n_done; ++i) p.done_out[i] = r.done_out[i];
+  p.n_done = r.n_done;
+  p.done_value = r.done_value;
   memcpy(p.root_L, r.root_L, sizeof p.root_L);
   memcpy(p.root_first, r.root_first, sizeof p.root_first);
   if (r.tree_L >= 0) {
@@ -1033,6 +1177,12 @@ void fill_vec_params(FoldParams &p, const FoldReq &r, unsigned long long e0,
     memcpy(p.present, r.present, nodes);
   }
 }
+
+// gated instantiations exist only for the combine's programs over fp32
+// pool slots (canonical trees of at most 64 leaves)
+template <typename A, typename Prog> struct Gatable { static constexpr bool value = false; };
+template <int L> struct Gatable<float, ProgTree<L>> { static constexpr bool value = true; };
+template <int L> struct Gatable<float, ProgFull<L>> { static constexpr bool value = true; };
 
 template <typename A, typename Prog>
 int launch_direct_p(const FoldReq &r, unsigned long long e0, unsigned long long nvec,
@@ -1043,6 +1193,14 @@ int launch_direct_p(const FoldReq &r, unsigned long long e0, unsigned long long 
   unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)sms * 8));
   if (r.max_ctas > 0) blocks = std::min<unsigned long long>(blocks, (unsigned long long)r.max_ctas * 4);
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if constexpr (Gatable<A, Prog>::value) {
+    if (r.gate_mask) {
+      fold_direct_kernel<A, Prog, true><<<(unsigned)blocks, 256, 0, st>>>(p);
+      CK(cudaGetLastError());
+      return RCV_OK;
+    }
+  }
+  if (r.gate_mask) return set_err(RCV_EINVAL, "gated launch of a program without a gated kernel");
   fold_direct_kernel<A, Prog><<<(unsigned)blocks, 256, 0, st>>>(p);
   CK(cudaGetLastError());
   return RCV_OK;
@@ -1092,6 +1250,11 @@ int launch_tma_p(const FoldReq &r, const TmaGeom &g, unsigned long long e0,
   p.stages = g.stages;
   p.vpt = g.vpt;
   auto kern = fold_tma_kernel<A, Prog>;
+  if constexpr (Gatable<A, Prog>::value) {
+    if (r.gate_mask) kern = fold_tma_kernel<A, Prog, true>;
+  }
+  if (r.gate_mask && kern == fold_tma_kernel<A, Prog>)
+    return set_err(RCV_EINVAL, "gated launch of a program without a gated kernel");
   {
     // one attribute call per (kernel, device, size): it is not free
     static std::mutex mu;
@@ -1223,6 +1386,17 @@ int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int s
     if (rc) return rc;
   }
   return RCV_OK;
+}
+
+// Whether run_fold issues exactly one vector launch for r over numel
+// elements (no scalar head or tail): the condition for a flag-gated launch.
+bool single_vec_launch(const FoldReq &r, size_t numel) {
+  if (numel == 0 || r.n_in == 0 || r.n_out == 0 || r.n_roots > 0) return false;
+  if (r.acc_dt != RCV_F32 || r.tree_L < 0 || r.tree_L > 6) return false;  // Gatable programs
+  if (getenv("RCV_TREE_EVAL") && atoi(getenv("RCV_TREE_EVAL")) == 1) return false;
+  for (int i = 0; i < r.n_in; ++i)
+    if (r.in_dt[i] != RCV_F32) return false;
+  return common_head(r) == 0 && numel % 8 == 0;
 }
 
 int check_dtype(int acc_dt, int in_dt) {
@@ -1831,6 +2005,15 @@ struct rcv_ctx {
     int es = 4;
   };
   std::vector<Pending> pending;  // combined buckets awaiting the local broadcast
+  // gated runtime (RCV_GATE, default on): per-call ready / done sequences in
+  // the flag arrays instead of a barrier kernel between pre-reduce and combine
+  bool gate = false;
+  // local broadcasts on their own stream, right behind each barrier
+  // (RCV_BCAST_STREAM), instead of between pre-reduces on the side stream
+  cudaStream_t bstream = nullptr;
+  cudaEvent_t ev_bcast = nullptr;  // bstream's tail, for a side-stream flush after it
+  bool bstream_dirty = false;      // bstream holds broadcasts the side has not waited for
+  unsigned int *d_gate_counter = nullptr;  // CTAs of the running gated combine
   unsigned int *d_counter = nullptr;  // fused kernel: phase-A CTAs done per slice
   unsigned long long fseq = 0;        // fused kernel: ready-flag sequence
   bool fused_in_step = false;
@@ -1874,6 +2057,7 @@ struct rcv_plan {
   int variant = 0, comb_variant = 0;
   uint64_t live_mask = 0;
   bool participate = false;
+  bool perfect = false;  // one cover node per live rank (the failure-free layout)
   int remote_in = 0, remote_out = 0;
 };
 
@@ -1931,10 +2115,85 @@ int ctx_flush(rcv_ctx *c, cudaStream_t st, long long upto) {
 
 extern "C" {
 
+}  // extern "C"
+
+namespace {
+
+// Load every kernel of this library's module on the current device.  Under
+// CUDA lazy loading (the default) the first launch of a kernel may need a
+// context synchronisation; if a flag-gated combine is already spinning for a
+// signal that kernel is to produce, that is a deadlock (broken only by the
+// wait's timeout).  So the runtime loads all of its kernels up front, once
+// per device, before any gated launch.
+int preload_module_kernels() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  for (int d : done)
+    if (d == dev) return RCV_OK;
+  typedef CUresult (*GetModule)(CUmodule *, CUfunction);
+  typedef CUresult (*Count)(unsigned int *, CUmodule);
+  typedef CUresult (*Enum)(CUfunction *, unsigned int, CUmodule);
+  typedef CUresult (*Load)(CUfunction);
+  typedef CUresult (*SetAttr)(CUfunction, CUfunction_attribute, int);
+  GetModule get_module = nullptr;
+  SetAttr set_attr = nullptr;
+  Count count = nullptr;
+  Enum enumerate = nullptr;
+  Load load = nullptr;
+  struct {
+    const char *name;
+    void **fn;
+  } eps[] = {{"cuFuncGetModule", (void **)&get_module},
+             {"cuModuleGetFunctionCount", (void **)&count},
+             {"cuModuleEnumerateFunctions", (void **)&enumerate},
+             {"cuFuncLoad", (void **)&load},
+             {"cuFuncSetAttribute", (void **)&set_attr}};
+  for (auto &e : eps) {
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint(e.name, e.fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !*e.fn) return set_err(RCV_ECUDA, "%s unavailable", e.name);
+  }
+  cudaFunction_t f0 = nullptr;
+  CK(cudaGetFuncBySymbol(&f0, (const void *)gate_kernel));
+  CUmodule mod = nullptr;
+  if (get_module(&mod, (CUfunction)f0) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuFuncGetModule");
+  unsigned int n = 0;
+  if (count(&n, mod) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuModuleGetFunctionCount");
+  std::vector<CUfunction> fs(n);
+  if (n && enumerate(fs.data(), n, mod) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuModuleEnumerateFunctions");
+  // One shared-memory carveout for every kernel: the runtime runs DIRECT
+  // (register-only) and TMA (up to ~200 KB of smem) kernels concurrently on
+  // two streams, and an SM configured for a large L1 by a DIRECT CTA cannot
+  // take a TMA CTA until it drains (measured: a queued broadcast idling
+  // 70 us behind a combine).  DIRECT loads bypass L1 (no_allocate), so they
+  // lose nothing to the max-shared split.  RCV_CARVEOUT=-1 keeps the default.
+  const char *cv = getenv("RCV_CARVEOUT");
+  const int carveout = cv ? atoi(cv) : 100;
+  for (CUfunction f : fs) {
+    if (load(f) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuFuncLoad");
+    if (carveout >= 0 &&
+        set_attr(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, carveout) != CUDA_SUCCESS)
+      return set_err(RCV_ECUDA, "cuFuncSetAttribute(carveout)");
+  }
+  done.push_back(dev);
+  return RCV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer_flags,
                    uint32_t *status, uint64_t timeout_ns, rcv_ctx **out) {
   if (n_ranks < 1 || n_ranks > 32 || me < 0 || me >= n_ranks)
     return set_err(RCV_ERANGE, "ctx: n_ranks %d me %d", n_ranks, me);
+  {
+    const int rc = preload_module_kernels();
+    if (rc) return rc;
+  }
   rcv_ctx *c = new rcv_ctx();
   c->n_ranks = n_ranks;
   c->me = me;
@@ -1964,6 +2223,20 @@ int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer
   for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->ev_arrived[i], cudaEventDisableTiming));
   CK(cudaMalloc(&c->d_counter, FUSED_MAX_SLICES * sizeof(unsigned int)));
   CK(cudaMemset(c->d_counter, 0, FUSED_MAX_SLICES * sizeof(unsigned int)));
+  CK(cudaMalloc(&c->d_gate_counter, sizeof(unsigned int)));
+  CK(cudaMemset(c->d_gate_counter, 0, sizeof(unsigned int)));
+  {
+    const char *g = getenv("RCV_GATE");
+    const char *fz = getenv("RCV_FUSED");
+    const char *ce = getenv("RCV_CE_GATHER");
+    c->gate = (g ? atoi(g) != 0 : false) && !(fz && atoi(fz)) && !(ce && atoi(ce));
+    const char *bs = getenv("RCV_BCAST_STREAM");
+    if ((bs ? atoi(bs) != 0 : true) && !c->gate && !(ce && atoi(ce)))
+    {
+      CK(cudaStreamCreateWithPriority(&c->bstream, cudaStreamNonBlocking, lo_pri));
+      CK(cudaEventCreateWithFlags(&c->ev_bcast, cudaEventDisableTiming));
+    }
+  }
   *out = c;
   return RCV_OK;
 }
@@ -1980,6 +2253,12 @@ int rcv_ctx_destroy(rcv_ctx *c) {
   cudaEventDestroy(c->ev_ready);
   for (int i = 0; i < 3; ++i) cudaEventDestroy(c->ev_arrived[i]);
   cudaFree(c->d_counter);
+  cudaFree(c->d_gate_counter);
+  if (c->bstream) {
+    cudaStreamSynchronize(c->bstream);
+    cudaStreamDestroy(c->bstream);
+    cudaEventDestroy(c->ev_bcast);
+  }
   cudaStreamDestroy(c->side);
   delete c;
   return RCV_OK;
@@ -2016,6 +2295,11 @@ int rcv_ctx_finish(rcv_ctx *c, uint64_t live_mask, int participate, void *main_s
     // the side stream's tail (broadcasts) joins the caller's stream
     CK(cudaEventRecord(c->ev_ready, c->side));
     CK(cudaStreamWaitEvent(st, c->ev_ready, 0));
+    if (c->bstream_dirty) {
+      CK(cudaEventRecord(c->ev_ready, c->bstream));
+      CK(cudaStreamWaitEvent(st, c->ev_ready, 0));
+      c->bstream_dirty = false;
+    }
   }
   int rc = ctx_barrier(c, live_mask, participate != 0, st);
   if (rc) return rc;
@@ -2041,6 +2325,18 @@ static int env_ctas(const char *name, int sms, double dflt_frac) {
 // 2.60 ms/step (failure-free 2.27 -> 1.91, degraded 3.59 -> 3.28); N=2
 // neutral.  RCV_COMB_CTAS / RCV_PRE_CTAS override (0: uncapped).
 constexpr double kCombShare = 0.35, kPreShare = 0.65;
+// A perfect cover (one node per live rank, the failure-free layout) moves
+// the fewest NVLink bytes per HBM byte of pre-reduce, so the pre-reduce sets
+// the cadence.  Giving it the larger share helped while the broadcasts ran
+// on the side stream (N=4 failure-free 2.00 -> 1.79 ms at 0.2 / 0.8) but not
+// once they moved to their own stream (1.64 vs 1.70), so the default keeps
+// one split; RCV_PERFECT_SHARE sets the combine share of perfect covers.
+double comb_share(const rcv_plan_desc *d) {
+  const bool perfect = d->n_comb > 0 && d->n_comb == d->slice_nr;
+  const char *v = getenv("RCV_PERFECT_SHARE");
+  const double f = v ? atof(v) : 0.0;  // measured best off once bstream is on
+  return perfect && f > 0 ? f : kCombShare;
+}
 
 int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
   rcv_plan *p = new rcv_plan();
@@ -2051,6 +2347,7 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
   if (const char *cv = getenv("RCV_COMB_VARIANT")) p->comb_variant = atoi(cv);  // experiments
   p->live_mask = d->live_mask;
   p->participate = d->participate != 0;
+  p->perfect = d->n_comb > 0 && d->n_comb == d->slice_nr;
   p->remote_in = d->remote_in;
   p->remote_out = d->remote_out;
   int off = 0;
@@ -2063,7 +2360,7 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       delete p;
       return rc;
     }
-    r.max_ctas = env_ctas("RCV_PRE_CTAS", ctx->sms, kPreShare);
+    r.max_ctas = env_ctas("RCV_PRE_CTAS", ctx->sms, 1.0 - comb_share(d));
     p->pre.push_back(r);
     p->pre_count.push_back(d->pre_counts[i]);
     off += d->pre_counts[i];
@@ -2103,7 +2400,7 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       r.n_out = d->n_pre;
       r.n_roots = d->n_pre;
       r.acc_dt = d->acc_dtype;
-      r.max_ctas = env_ctas("RCV_PRE_CTAS", ctx->sms, kPreShare);
+      r.max_ctas = env_ctas("RCV_PRE_CTAS", ctx->sms, 1.0 - comb_share(d));
       p->has_forest = true;
       p->forest_count = k;
     }
@@ -2131,7 +2428,7 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       delete p;
       return rc;
     }
-    p->comb.max_ctas = env_ctas("RCV_COMB_CTAS", ctx->sms, kCombShare);
+    p->comb.max_ctas = env_ctas("RCV_COMB_CTAS", ctx->sms, comb_share(d));
     if (d->guarded) {
       // the combine reads live peers' partials: skip it once one timed out
       p->comb.guard = (const unsigned int *)ctx->bar.status;
@@ -2238,6 +2535,148 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
   return RCV_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+constexpr int kReadyBase = 128, kDoneBase = 160;  // flag slots (dist.FLAG_SLOTS >= 192)
+
+int launch_gate(rcv_ctx *c, cudaStream_t st, const GateParams &g) {
+  return timed(c, st, 1, 0, 0, 0, [&]() {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    gate_kernel<<<1, 32, 0, st>>>(g);
+    CK(cudaGetLastError());
+    return RCV_OK;
+  });
+}
+
+// Gated per-bucket schedule of call j (no barrier kernel, no cross-stream
+// events inside the step):
+//   side: broadcasts of calls <= j-3 -> pre-reduce(j) into pool set j%3 ->
+//         gate: release ready = j+1 to every live rank, then acquire every
+//         live rank's done >= j-1 (their combine of call j-2 has read pool
+//         set (j+1)%3 and stored its slices), so the side stream runs at most
+//         two calls ahead of the slowest combine
+//   main: combine(j), whose CTAs acquire ready >= j+1 from every live rank
+//         before the first load and whose last CTA releases done = j+1.
+// A combine that cannot run as one vector launch (ragged slice) or a timed
+// pass takes the explicit form: gate(wait ready) -> combine -> gate(done).
+int plan_bucket_gated(rcv_plan *p, size_t lo, size_t n, cudaStream_t main, cudaStream_t side) {
+  rcv_ctx *c = p->ctx;
+  if (!c->in_step) {
+    // leaves were produced on the caller's stream
+    c->in_step = true;
+    c->fused_in_step = false;
+    CK(cudaEventRecord(c->ev_main, main));
+    CK(cudaStreamWaitEvent(c->side, c->ev_main, 0));
+  }
+  const unsigned long long j = c->calls++;
+  const size_t set_off = (j % 3) * p->set_stride;
+  const int es = esize(p->has_comb ? p->comb.acc_dt : RCV_F32);
+  int rc = RCV_OK;
+  if (j >= 3 && (rc = ctx_flush(c, side, (long long)j - 3))) return rc;
+  if (!p->participate) return RCV_OK;
+  bool forest_done = false;
+  if (p->has_forest && n % 64 == 0) {
+    FoldReq r = p->forest;
+    shift(r, lo, set_off);
+    if (common_head(r) == 0) {
+      const double bytes = (double)(p->forest_count + r.n_out) * n * esize(r.acc_dt);
+      if ((rc = timed(c, side, 0, bytes, 0, 0, [&]() { return run_fold(r, n, p->variant, side, c->sms); })))
+        return rc;
+      forest_done = true;
+    }
+  }
+  for (size_t i = 0; i < p->pre.size() && !forest_done; ++i) {
+    FoldReq r = p->pre[i];
+    shift(r, lo, set_off);
+    const double bytes = (double)(p->pre_count[i] + 1) * n * esize(r.acc_dt);
+    if ((rc = timed(c, side, 0, bytes, 0, 0, [&]() { return run_fold(r, n, p->variant, side, c->sms); })))
+      return rc;
+  }
+  const unsigned int live = (unsigned int)p->live_mask;
+  GateParams ready;
+  memset(&ready, 0, sizeof ready);
+  for (int r = 0; r < c->n_ranks; ++r)
+    if ((live >> r) & 1u) ready.signal[ready.n_signal++] = c->bar.peer[r] + kReadyBase + c->me;
+  ready.signal_value = j + 1;
+  if (j >= 2) {
+    ready.wait_flags = c->bar.local + kDoneBase;
+    ready.wait_value = j - 1;
+    ready.wait_mask = live;
+  }
+  ready.status = c->bar.status;
+  ready.timeout_ns = c->bar.timeout_ns;
+  if ((rc = launch_gate(c, side, ready))) return rc;
+
+  GateParams done;
+  memset(&done, 0, sizeof done);
+  for (int r = 0; r < c->n_ranks; ++r)
+    if ((live >> r) & 1u) done.signal[done.n_signal++] = c->bar.peer[r] + kDoneBase + c->me;
+  done.signal_value = j + 1;
+  done.status = c->bar.status;
+  done.timeout_ns = c->bar.timeout_ns;
+  size_t a = 0, z = 0;
+  if (p->has_comb) {
+    const size_t units = (n + 63) / 64;
+    a = std::min(n, p->slice_at(units, p->slice_q));
+    z = std::min(n, p->slice_at(units, p->slice_q + 1));
+  }
+  if (z > a) {
+    FoldReq r = p->comb;
+    shift(r, set_off + a, lo + a);
+    const double sl = (double)(z - a) * es;
+    const double local = (double)(r.n_in - p->remote_in + r.n_out - p->remote_out) * sl;
+    if (!c->timing && single_vec_launch(r, z - a)) {
+      r.gate_flags = c->bar.local + kReadyBase;
+      r.gate_value = j + 1;
+      r.gate_mask = live;
+      r.gate_status = c->bar.status;
+      r.gate_timeout_ns = c->bar.timeout_ns;
+      r.done_counter = c->d_gate_counter;
+      for (int i = 0; i < done.n_signal; ++i) r.done_out[i] = done.signal[i];
+      r.n_done = done.n_signal;
+      r.done_value = j + 1;
+      // waiting CTAs hold their SMs: leave at least half of the GPU to the
+      // pre-reduce they wait for
+      const int cap = std::max(1, c->sms / 2);
+      if (r.max_ctas <= 0 || r.max_ctas > cap) r.max_ctas = cap;
+      rc = timed(c, main, 3, local, p->remote_in * sl, p->remote_out * sl,
+                 [&]() { return run_fold(r, z - a, p->comb_variant, main, c->sms); });
+      if (rc) return rc;
+    } else {
+      GateParams w;
+      memset(&w, 0, sizeof w);
+      w.wait_flags = c->bar.local + kReadyBase;
+      w.wait_value = j + 1;
+      w.wait_mask = live;
+      w.status = c->bar.status;
+      w.timeout_ns = c->bar.timeout_ns;
+      if ((rc = launch_gate(c, main, w))) return rc;
+      rc = timed(c, main, 3, local, p->remote_in * sl, p->remote_out * sl,
+                 [&]() { return run_fold(r, z - a, p->comb_variant, main, c->sms); });
+      if (rc) return rc;
+      if ((rc = launch_gate(c, main, done))) return rc;
+    }
+  } else if ((rc = launch_gate(c, main, done))) {
+    return rc;
+  }
+  if (p->has_bcast) {
+    rcv_ctx::Pending e;
+    e.req = p->bcast;
+    e.lo = lo;
+    e.n = n;
+    e.variant = p->variant;
+    e.call = j;
+    c->pending.push_back(e);
+  }
+  return RCV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int rcv_plan_destroy(rcv_plan *p) {
   delete p;
   return RCV_OK;
@@ -2292,6 +2731,7 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
     }
     return RCV_OK;
   }
+  if (c->gate) return plan_bucket_gated(p, lo, n, main, side);
   if (!c->in_step || c->fused_in_step) {
     // leaves were produced on the caller's stream (and, after fused
     // buckets, the pool sets they used are released only in stream order)
@@ -2308,9 +2748,20 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
   // broadcasts go here, off the main stream.
   const unsigned long long j = c->calls++;
   const size_t set_off = (j % 3) * p->set_stride;
+  // perfect covers (pre-reduce-bound) broadcast on their own stream right
+  // behind each barrier; fragmented ones (combine-bound) keep them on the
+  // side stream, off the SMs the NVLink-bound combine needs
+  // (profiles/r1f/schedule_ab.txt)
+  const bool bstream = c->bstream && !c->timing && p->perfect;
   if (j >= 2) {
     CK(cudaStreamWaitEvent(side, c->ev_arrived[(j - 2) % 3], 0));
-    if (j >= 3) {
+    if (j >= 3 && !bstream) {
+      if (c->bstream_dirty) {
+        // an earlier broadcast of the same bucket may still be on bstream
+        CK(cudaEventRecord(c->ev_bcast, c->bstream));
+        CK(cudaStreamWaitEvent(side, c->ev_bcast, 0));
+        c->bstream_dirty = false;
+      }
       int rc = ctx_flush(c, side, (long long)j - 3);
       if (rc) return rc;
     }
@@ -2342,6 +2793,14 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
   int rc = ctx_barrier(c, p->live_mask, p->participate, main);
   if (rc) return rc;
   CK(cudaEventRecord(c->ev_arrived[j % 3], main));
+  if (bstream && j >= 1) {
+    // passing barrier j proves every peer finished combine j-1: the buckets
+    // combined at calls <= j-1 are complete in this rank's primary
+    CK(cudaStreamWaitEvent(c->bstream, c->ev_arrived[j % 3], 0));
+    rc = ctx_flush(c, c->bstream, (long long)j - 1);
+    if (rc) return rc;
+    c->bstream_dirty = true;
+  }
   if (p->has_comb) {
     const size_t units = (n + 63) / 64;
     const size_t a = std::min(n, p->slice_at(units, p->slice_q));

@@ -50,8 +50,9 @@ from .policy import assign_roles, initial_state, policy_advancement
 
 
 # per-rank flag words in peer memory: [0, 64) the step barrier, [64, 128)
-# the fused kernel's per-producer ready sequence
-FLAG_SLOTS = 128
+# the fused kernel's per-producer ready sequence, [128, 160) the gated
+# runtime's "partials ready" and [160, 192) its "combine done" sequences
+FLAG_SLOTS = 192
 
 
 def fused_eligible(cover, slot_of, leaves, ranks, b, acc_code, aligned=True) -> bool:
@@ -288,7 +289,8 @@ class DistributedGradientCommit(GradientCommit):
         self.pool_slots = pool_slots
         self.real_kill = real_kill
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
-        self.timeout_ns = int(barrier_timeout_s * 1e9)
+        # RCV_TIMEOUT_S overrides every bounded wait (debugging hangs)
+        self.timeout_ns = int(float(os.environ.get("RCV_TIMEOUT_S", barrier_timeout_s)) * 1e9)
         if real_kill:
             # VMM memory: survivors' mappings outlive a dead exporter
             vb = VmmBuffers(self.rank, self.world, group)
