@@ -1072,6 +1072,9 @@ struct FoldReq {
   uint8_t root_first[8] = {};
   int8_t node_in[2 * RCV_MAX_IN - 1];
   uint8_t present[2 * RCV_MAX_IN - 1];
+  // fp32 inputs evaluated as 8-element vectors (two 16-byte loads per input):
+  // halves the per-byte cost of a branchy evaluator's control flow
+  bool wide32 = false;
   // flag gate of a single vector launch (FoldParams::gate_*), runtime only
   const unsigned long long *gate_flags = nullptr;
   unsigned long long gate_value = 0;
@@ -1343,7 +1346,7 @@ int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int s
     return RCV_OK;
   }
   const bool f64 = r.acc_dt == RCV_F64;
-  bool wide = false;  // fp32 over bf16 inputs: 8-element vectors (float8)
+  bool wide = r.wide32 && !f64;  // fp32 over bf16 inputs: 8-element vectors (float8)
   for (int i = 0; i < r.n_in && !f64; ++i) wide |= r.in_dt[i] == RCV_BF16;
   const int E = f64 ? 2 : (wide ? 8 : 4);
   int h = variant == RCV_VARIANT_SCALAR ? -1 : common_head(r);
@@ -1392,7 +1395,7 @@ int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int s
 // elements (no scalar head or tail): the condition for a flag-gated launch.
 bool single_vec_launch(const FoldReq &r, size_t numel) {
   if (numel == 0 || r.n_in == 0 || r.n_out == 0 || r.n_roots > 0) return false;
-  if (r.acc_dt != RCV_F32 || r.tree_L < 0 || r.tree_L > 6) return false;  // Gatable programs
+  if (r.acc_dt != RCV_F32 || r.tree_L < 0 || r.tree_L > 6 || r.wide32) return false;  // Gatable programs
   if (getenv("RCV_TREE_EVAL") && atoi(getenv("RCV_TREE_EVAL")) == 1) return false;
   for (int i = 0; i < r.n_in; ++i)
     if (r.in_dt[i] != RCV_F32) return false;
@@ -2429,6 +2432,13 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       return rc;
     }
     p->comb.max_ctas = env_ctas("RCV_COMB_CTAS", ctx->sms, comb_share(d));
+    {
+      // RCV_WIDE_COMB: 0 off, 1 branchy trees (ProgTree: fragmented covers),
+      // 2 every combine
+      const char *w = getenv("RCV_WIDE_COMB");
+      const int wide = w ? atoi(w) : 1;
+      p->comb.wide32 = wide >= 2 || (wide == 1 && p->comb.full_L < 0);
+    }
     if (d->guarded) {
       // the combine reads live peers' partials: skip it once one timed out
       p->comb.guard = (const unsigned int *)ctx->bar.status;

@@ -1,7 +1,7 @@
 #!/bin/bash
-# Runtime schedule A/B on a 4-GPU box: per-plan broadcast stream vs side stream
+# combine vector width A/B on a 4-GPU box
 OUT=gpurun_out; mkdir -p $OUT
-timeout 600 python -m pytest tests -m multigpu -q -x > $OUT/pytest_multi_bs.log 2>&1; echo "pytest multigpu rc=$?"
-tail -2 $OUT/pytest_multi_bs.log
-bash tools/gpu_envab.sh 4 "RCV_BCAST_STREAM=1" "RCV_BCAST_STREAM=0" "RCV_BCAST_STREAM=1"
-bash tools/gpu_envab.sh 2 "RCV_BCAST_STREAM=1" "RCV_BCAST_STREAM=0"
+timeout 600 python -m pytest tests -m multigpu -q -x > $OUT/pytest_multi_w.log 2>&1; echo "pytest multigpu rc=$?"
+tail -2 $OUT/pytest_multi_w.log
+bash tools/gpu_envab.sh 2 "RCV_WIDE_COMB=1" "RCV_WIDE_COMB=0" "RCV_WIDE_COMB=2"
+bash tools/gpu_envab.sh 4 "RCV_WIDE_COMB=1" "RCV_WIDE_COMB=0" "RCV_WIDE_COMB=2"
