@@ -2330,14 +2330,14 @@ static int env_ctas(const char *name, int sms, double dflt_frac) {
 constexpr double kCombShare = 0.35, kPreShare = 0.65;
 // A perfect cover (one node per live rank, the failure-free layout) moves
 // the fewest NVLink bytes per HBM byte of pre-reduce, so the pre-reduce sets
-// the cadence.  Giving it the larger share helped while the broadcasts ran
-// on the side stream (N=4 failure-free 2.00 -> 1.79 ms at 0.2 / 0.8) but not
-// once they moved to their own stream (1.64 vs 1.70), so the default keeps
-// one split; RCV_PERFECT_SHARE sets the combine share of perfect covers.
+// the cadence and gets the larger share: 0.25 / 0.75 (N=2 failure-free
+// 2.31 -> 2.21 ms; N=4 1.64-1.66 ms at 0.25-0.35, within noise;
+// profiles/r1f/schedule_ab.txt).  RCV_PERFECT_SHARE sets the combine share
+// of perfect covers (0: the fragmented split).
 double comb_share(const rcv_plan_desc *d) {
   const bool perfect = d->n_comb > 0 && d->n_comb == d->slice_nr;
   const char *v = getenv("RCV_PERFECT_SHARE");
-  const double f = v ? atof(v) : 0.0;  // measured best off once bstream is on
+  const double f = v ? atof(v) : 0.25;
   return perfect && f > 0 ? f : kCombShare;
 }
 

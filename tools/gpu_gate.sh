@@ -1,7 +1,3 @@
 #!/bin/bash
-# combine vector width A/B on a 4-GPU box
-OUT=gpurun_out; mkdir -p $OUT
-timeout 600 python -m pytest tests -m multigpu -q -x > $OUT/pytest_multi_w.log 2>&1; echo "pytest multigpu rc=$?"
-tail -2 $OUT/pytest_multi_w.log
-bash tools/gpu_envab.sh 2 "RCV_WIDE_COMB=1" "RCV_WIDE_COMB=0" "RCV_WIDE_COMB=2"
-bash tools/gpu_envab.sh 4 "RCV_WIDE_COMB=1" "RCV_WIDE_COMB=0" "RCV_WIDE_COMB=2"
+# SM split for perfect covers at N=2 (pre-reduce HBM-bound)
+bash tools/gpu_envab.sh 2 "RCV_PERFECT_SHARE=0" "RCV_PERFECT_SHARE=0.2" "RCV_PERFECT_SHARE=0.25" "RCV_PERFECT_SHARE=0.15" "RCV_PERFECT_SHARE=0"
