@@ -2234,6 +2234,8 @@ int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer
     const char *ce = getenv("RCV_CE_GATHER");
     c->gate = (g ? atoi(g) != 0 : false) && !(fz && atoi(fz)) && !(ce && atoi(ce));
     const char *bs = getenv("RCV_BCAST_STREAM");
+    // not with the gate: gate + broadcast stream measured slower (N=4
+    // failure-free 1.75 vs 1.66 ms) and hung the multi-GPU tests
     if ((bs ? atoi(bs) != 0 : true) && !c->gate && !(ce && atoi(ce)))
     {
       CK(cudaStreamCreateWithPriority(&c->bstream, cudaStreamNonBlocking, lo_pri));
@@ -2584,7 +2586,17 @@ int plan_bucket_gated(rcv_plan *p, size_t lo, size_t n, cudaStream_t main, cudaS
   const size_t set_off = (j % 3) * p->set_stride;
   const int es = esize(p->has_comb ? p->comb.acc_dt : RCV_F32);
   int rc = RCV_OK;
-  if (j >= 3 && (rc = ctx_flush(c, side, (long long)j - 3))) return rc;
+  // perfect covers broadcast on their own stream behind a done-flag wait
+  // (as in the barrier runtime); fragmented ones on the side stream
+  const bool bstream = c->bstream && !c->timing && p->perfect;
+  if (j >= 3 && !bstream) {
+    if (c->bstream_dirty) {
+      CK(cudaEventRecord(c->ev_bcast, c->bstream));
+      CK(cudaStreamWaitEvent(side, c->ev_bcast, 0));
+      c->bstream_dirty = false;
+    }
+    if ((rc = ctx_flush(c, side, (long long)j - 3))) return rc;
+  }
   if (!p->participate) return RCV_OK;
   bool forest_done = false;
   if (p->has_forest && n % 64 == 0) {
@@ -2670,6 +2682,20 @@ int plan_bucket_gated(rcv_plan *p, size_t lo, size_t n, cudaStream_t main, cudaS
     }
   } else if ((rc = launch_gate(c, main, done))) {
     return rc;
+  }
+  if (bstream && j >= 1 && !c->pending.empty()) {
+    // every live rank's combine of call j-1 is done: the buckets combined
+    // at calls <= j-1 are complete in this rank's primary
+    GateParams w;
+    memset(&w, 0, sizeof w);
+    w.wait_flags = c->bar.local + kDoneBase;
+    w.wait_value = j;
+    w.wait_mask = live;
+    w.status = c->bar.status;
+    w.timeout_ns = c->bar.timeout_ns;
+    if ((rc = launch_gate(c, c->bstream, w))) return rc;
+    if ((rc = ctx_flush(c, c->bstream, (long long)j - 1))) return rc;
+    c->bstream_dirty = true;
   }
   if (p->has_bcast) {
     rcv_ctx::Pending e;
