@@ -409,7 +409,7 @@ def run_ours(args):
                    "fail_step": fail_step, "placement": "8 replicas on 1 GPU" if world == 1
                    else "%d replicas per rank, NVLink P2P" % (W // world), "l2": "inputs 15.9 GB >> 126 MB L2",
                    "parallelism": "dp8-sim"},
-        "roofline": roofline(dom, per_kind, peak, peak_kind),
+        "roofline": roofline(dom, per_kind, peak, peak_kind, world),
         "kernels": per_kind,
         "kernels_degraded": per_kind_deg or None,
         # masked-allreduce algorithmic bandwidth: gradient bytes committed
@@ -470,15 +470,20 @@ def summarise_kernels(recs):
     return kinds, per_kind
 
 
-def roofline(dom, per_kind, peak, peak_kind):
+def roofline(dom, per_kind, peak, peak_kind, world=1):
     if dom is None:
         return None
     k = per_kind[dom]
     if dom == "combine" and (k["nvlink_gbs_per_direction"] or 0) > 0:
         ach = k["nvlink_gbs_per_direction"]
+        # the per-kernel pass runs failure-free steps: one cover node per
+        # rank, a perfect tree of world leaves, which AUTO runs DIRECT
         return {"bound": "nvlink", "achieved": ach, "peak": NVLINK_PEAK, "unit": "GB/s",
                 "frac": ach / NVLINK_PEAK, "traffic": None, "peak_kind": "measured peer copy",
-                "kernel": "fold_tma_kernel combine (rcv_tree_commit over peer pointers)",
+                "kernel": "fold_direct_kernel<float, ProgFull<%d>> combine over peer pointers "
+                          "(failure-free cover; degraded covers run fold_tma_kernel<F8, ProgTree<L>>, "
+                          "see kernels_degraded)" % max(0, world.bit_length() - 1),
+                "mean_launch_us": k["mean_launch_us"], "launches_timed": k["launches"],
                 "hbm_gbs": k["hbm_gbs"]}
     return {"bound": "hbm", "achieved": k["hbm_gbs"], "peak": peak, "unit": "GB/s",
             "frac": k["hbm_gbs"] / peak if k["hbm_gbs"] else None,

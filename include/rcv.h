@@ -229,13 +229,21 @@ int rcv_barrier(uint64_t *local_flags, void *const *peer_flags, int n, int me,
 
 /* ---- native per-bucket runtime for the multi-process commit --------------
  * One context per rank (flags, status, a side stream for pre-reduces, the
- * barrier sequence, the pending local broadcast); one plan per leaf cover
+ * barrier sequence, the pending local broadcasts); one plan per leaf cover
  * (prepared fold requests: validated once, relaunched per bucket).  A bucket
  * then costs the host one call: rcv_plan_bucket enqueues
- *   side stream: wait(pool set free) -> pre-reduce nodes -> record(ready)
- *   main stream: wait(ready) -> barrier -> broadcast(previous bucket) ->
- *                record(other set free) -> combine(owner slice)
- * and rcv_ctx_finish closes the step (barrier + last broadcast). */
+ *   side stream:  wait(pool set free) -> [broadcasts, fragmented covers] ->
+ *                 pre-reduce nodes -> record(ready)
+ *   main stream:  wait(ready) -> barrier -> record(arrived) -> combine(owner slice)
+ *   bcast stream: wait(arrived) -> broadcasts of the buckets combined before
+ *                 (perfect covers: one node per live rank)
+ * and rcv_ctx_finish closes the step (barrier + last broadcasts).
+ * RCV_GATE=1 (opt-in) replaces the barrier by per-call ready/done flags the
+ * combine kernel acquires/releases itself.  rcv_ctx_create loads every
+ * kernel of the library up front (CUDA lazy loading could otherwise need a
+ * context sync while a kernel waits on a peer's flag).
+ * local_flags / peer_flags: 192 uint64 per rank ([0,64) barrier, [64,128)
+ * fused kernel, [128,160) gate ready, [160,192) gate done). */
 typedef struct rcv_ctx rcv_ctx;
 typedef struct rcv_plan rcv_plan;
 
