@@ -279,6 +279,9 @@ struct FoldParams {
   unsigned long long *done_out[32];
   int n_done;
   unsigned long long done_value;
+  // launched as a programmatic dependent (PDL) of the previous kernel in its
+  // stream: wait for that grid's completion and memory before any access
+  int pdl;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -478,6 +481,7 @@ template <typename A, typename Prog, bool kGate = false>
 __global__ void __launch_bounds__(256)
     fold_direct_kernel(const __grid_constant__ FoldParams p) {
   using V = typename VecT<A>::V;
+  if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   if constexpr (kGate) {
     // the loads below are L1::no_allocate, so no line of a pool slot can be
     // cached on this SM before its producer's ready flag was acquired
@@ -548,6 +552,8 @@ template <typename A, typename Prog, bool kGate = false>
 __global__ void __launch_bounds__(TMA_THREADS)
     fold_tma_kernel(const __grid_constant__ FoldParams p) {
   using V = typename VecT<A>::V;
+  // returns at once unless the grid was launched as a PDL dependent
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const bool guarded = p.guard && (*p.guard & p.guard_mask);
   if (!kGate && guarded) return;  // uniform: before any barrier
   extern __shared__ __align__(128) unsigned char smem[];
@@ -827,6 +833,9 @@ struct BarrierParams {
 
 __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   const int t = threadIdx.x;
+  // a PDL-launched combine behind this barrier may start its CTAs now; they
+  // block in griddepcontrol.wait until this grid has completed
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // a peer that already timed out is dead: never signal or wait on it again
   const unsigned int dead = *(volatile const unsigned int *)p.status;
   const bool peer = t < p.n && t != p.me && ((p.live >> t) & 1ull) && !((dead >> t) & 1u);
@@ -1075,6 +1084,7 @@ struct FoldReq {
   // fp32 inputs evaluated as 8-element vectors (two 16-byte loads per input):
   // halves the per-byte cost of a branchy evaluator's control flow
   bool wide32 = false;
+  bool pdl = false;  // launch as a programmatic dependent (cudaLaunchKernelEx)
   // flag gate of a single vector launch (FoldParams::gate_*), runtime only
   const unsigned long long *gate_flags = nullptr;
   unsigned long long gate_value = 0;
@@ -1163,6 +1173,7 @@ void fill_vec_params(FoldParams &p, const FoldReq &r, unsigned long long e0,
   p.guard = r.guard;
   p.guard_mask = r.guard_mask;
   p.n_roots = r.n_roots;
+  p.pdl = r.pdl;
   p.gate_flags = r.gate_flags;
   p.gate_value = r.gate_value;
   p.gate_mask = r.gate_mask;
@@ -1179,6 +1190,24 @@ void fill_vec_params(FoldParams &p, const FoldReq &r, unsigned long long e0,
     memcpy(p.node_in, r.node_in, nodes);
     memcpy(p.present, r.present, nodes);
   }
+}
+
+// Launch as a programmatic dependent of the previous kernel in `st` (PDL):
+// the grid may be scheduled while that kernel still runs and waits for it
+// in griddepcontrol.wait (FoldParams::pdl).
+cudaError_t launch_pdl(void (*kern)(FoldParams), unsigned blocks, unsigned threads, size_t smem,
+                       cudaStream_t st, const FoldParams &p) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 // gated instantiations exist only for the combine's programs over fp32
@@ -1204,6 +1233,10 @@ int launch_direct_p(const FoldReq &r, unsigned long long e0, unsigned long long 
     }
   }
   if (r.gate_mask) return set_err(RCV_EINVAL, "gated launch of a program without a gated kernel");
+  if (r.pdl) {
+    CK(launch_pdl(fold_direct_kernel<A, Prog>, (unsigned)blocks, 256, 0, st, p));
+    return RCV_OK;
+  }
   fold_direct_kernel<A, Prog><<<(unsigned)blocks, 256, 0, st>>>(p);
   CK(cudaGetLastError());
   return RCV_OK;
@@ -1279,6 +1312,10 @@ int launch_tma_p(const FoldReq &r, const TmaGeom &g, unsigned long long e0,
       1, std::min<unsigned long long>(ntiles, (unsigned long long)sms * g.ctas_per_sm));
   if (r.max_ctas > 0) blocks = std::min<unsigned long long>(blocks, (unsigned long long)r.max_ctas);
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (r.pdl) {
+    CK(launch_pdl(kern, (unsigned)blocks, TMA_THREADS, g.smem, st, p));
+    return RCV_OK;
+  }
   kern<<<(unsigned)blocks, TMA_THREADS, g.smem, st>>>(p);
   CK(cudaGetLastError());
   return RCV_OK;
@@ -1400,6 +1437,16 @@ bool single_vec_launch(const FoldReq &r, size_t numel) {
   for (int i = 0; i < r.n_in; ++i)
     if (r.in_dt[i] != RCV_F32) return false;
   return common_head(r) == 0 && numel % 8 == 0;
+}
+
+// run_fold issues exactly one vector launch (any program, any dtype)
+bool single_vec_launch_any(const FoldReq &r, size_t numel) {
+  if (numel == 0 || r.n_in == 0 || r.n_out == 0) return false;
+  const bool f64 = r.acc_dt == RCV_F64;
+  bool wide = r.wide32 && !f64;
+  for (int i = 0; i < r.n_in && !f64; ++i) wide |= r.in_dt[i] == RCV_BF16;
+  const size_t E = f64 ? 2 : (wide ? 8 : 4);
+  return common_head(r) == 0 && numel % (2 * E) == 0;
 }
 
 int check_dtype(int acc_dt, int in_dt) {
@@ -2013,6 +2060,7 @@ struct rcv_ctx {
   bool gate = false;
   // local broadcasts on their own stream, right behind each barrier
   // (RCV_BCAST_STREAM), instead of between pre-reduces on the side stream
+  bool pdl = false;  // combine launched as a PDL dependent of its barrier (RCV_PDL=1)
   cudaStream_t bstream = nullptr;
   cudaEvent_t ev_bcast = nullptr;  // bstream's tail, for a side-stream flush after it
   bool bstream_dirty = false;      // bstream holds broadcasts the side has not waited for
@@ -2233,6 +2281,8 @@ int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer
     const char *fz = getenv("RCV_FUSED");
     const char *ce = getenv("RCV_CE_GATHER");
     c->gate = (g ? atoi(g) != 0 : false) && !(fz && atoi(fz)) && !(ce && atoi(ce));
+    const char *pd = getenv("RCV_PDL");
+    c->pdl = pd ? atoi(pd) != 0 : false;  // measured neutral (schedule_ab.txt 8.)
     const char *bs = getenv("RCV_BCAST_STREAM");
     // not with the gate: gate + broadcast stream measured slower (N=4
     // failure-free 1.75 vs 1.66 ms) and hung the multi-GPU tests
@@ -2844,6 +2894,10 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
     if (z > a) {
       FoldReq r = p->comb;
       shift(r, set_off + a, lo + a);
+      // PDL behind the barrier (RCV_PDL=1, opt-in), one vector launch
+      // only: a scalar head would sit between the barrier and the body
+      r.pdl = c->pdl && !c->timing && p->participate &&
+              __builtin_popcountll(p->live_mask) >= 2 && single_vec_launch_any(r, z - a);
       const double sl = (double)(z - a) * es;
       const double local = (double)(r.n_in - p->remote_in + r.n_out - p->remote_out) * sl;
       rc = timed(c, main, 3, local, p->remote_in * sl, p->remote_out * sl,
