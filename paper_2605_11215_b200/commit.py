@@ -28,6 +28,13 @@ changes only the data plane:
   a rewind is a no-op, and a stale bucket is recovered by re-running the
   launch over the repaired membership.  A dead replica's
   buffers are never read: its microbatches drop out of the leaf set.
+* **Committed buckets survive.**  A bucket whose data phase already ran in
+  this step over the same microbatch index set holds the canonical tree of
+  the same leaf values, so its re-reduce (the second pass after a
+  boundary) keeps the protocol call and its accounting but launches
+  nothing: only the work the dead replica had not committed is redone
+  (north star).  Off in real-kill mode, where a guarded combine may have
+  skipped itself, and with RCV_REUSE=0.
 
 Leaves come from a caller-supplied ``leaf(m, rid)`` returning the 1-D CUDA
 gradient of microbatch m as computed on replica rid (in the bench: synthetic
@@ -150,6 +157,13 @@ class GradientCommit:
         _lib.enable_peer_access(sorted({d.index for d in self.placement.values()}))
 
     # ---- data plane ----
+
+    def _reuse_committed(self) -> bool:
+        """Whether a bucket committed earlier in the step over the same leaf
+        index set may keep its outputs instead of being relaunched."""
+        import os
+        return os.environ.get("RCV_REUSE", "1") not in ("", "0") and \
+            not getattr(self, "real_kill", False)
 
     def _holds(self, rid: int) -> bool:
         """Whether this process holds replica rid's buffers (all of them in
@@ -389,9 +403,17 @@ class GradientCommit:
             leaf_cache[0], leaf_cache[1] = key, lv
             return lv
 
+        committed_keys: Dict[int, frozenset] = {}
+        reuse = self._reuse_committed()
+
         def reduce(k: int) -> WorkResult:
             def data():
-                cnt["launches"] += self._reduce_bucket(k, collect())
+                lv = collect()
+                keys = frozenset(lv)
+                if reuse and committed_keys.get(k) == keys:
+                    return  # same index set, same leaf bits: already committed
+                cnt["launches"] += self._reduce_bucket(k, lv)
+                committed_keys[k] = keys
             return comm.ulfm_collective(data)
 
         def on_failure(work: WorkResult) -> None:
