@@ -147,3 +147,35 @@ def test_engine_multidevice_placement():
     for r in eng.comm.members:
         torch.cuda.synchronize(place[r])
         assert eng.grads[r].cpu().numpy().tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("bucket", [0, 3, 5])
+def test_committed_buckets_survive_boundary(monkeypatch, bucket):
+    """A during_sync death at `bucket` sends the step through a boundary and
+    a second pass.  Buckets committed before the death keep their outputs
+    (same microbatch index set, same leaf bits) instead of being relaunched;
+    the committed gradient and the accounting equal the relaunching path's
+    and the failure-free canonical tree bit for bit."""
+    w, g, k = 4, 2, 6
+    b = w * g
+    numel = 64 * k * 3 + 40
+    host, dev = _leaves(b, numel, 77 + bucket)
+    want = fold.canonical_tree(dict(enumerate(host)), b) / np.float32(b)
+    outs = {}
+    for reuse in ("1", "0"):
+        monkeypatch.setenv("RCV_REUSE", reuse)
+        eng = GradientCommit(numel, w, g, k)
+        out = eng.step(0, lambda m, rid: dev[m], Scripted([("during_sync", bucket, [2])]))
+        torch.cuda.synchronize()
+        for rid in eng.comm.members:
+            assert eng.grads[rid].cpu().numpy().tobytes() == want.tobytes(), (reuse, rid)
+        outs[reuse] = out
+    a, z = outs["1"], outs["0"]
+    for f in ("contributions", "contrib_total", "events", "bucket_epochs", "reduces",
+              "rewinds", "passes", "roles"):
+        assert getattr(a, f) == getattr(z, f), f
+    # losing one of 4 replicas mid-commit crosses the boundary: the
+    # relaunching path commits every bucket again in the second pass, reuse
+    # relaunches only the failed bucket and those after it
+    assert a.boundary_crossed and z.boundary_crossed
+    assert z.launches - a.launches == bucket
