@@ -288,6 +288,9 @@ typedef struct {
                                     bucket (every live rank must agree; needs
                                     fp32, <= 8 perfect local nodes, <= 64
                                     local leaves, n_leaves <= 64) */
+  const uint32_t *slice_w;       /* slice_nr owner-slice weights in slice
+                                    order (NULL: equal slices); every live
+                                    rank must pass the same weights */
 } rcv_plan_desc;
 
 int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *desc, rcv_plan **out);

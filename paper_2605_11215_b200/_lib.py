@@ -63,6 +63,7 @@ class PlanDesc(ctypes.Structure):
         ("live_mask", ctypes.c_uint64), ("participate", ctypes.c_int),
         ("remote_in", ctypes.c_int), ("remote_out", ctypes.c_int),
         ("guarded", ctypes.c_int), ("fused", ctypes.c_int),
+        ("slice_w", ctypes.POINTER(ctypes.c_uint32)),
     ]
 
 

@@ -2094,8 +2094,12 @@ struct rcv_plan {
   bool has_comb = false;
   FoldReq comb;
   int slice_q = 0, slice_nr = 1;
+  std::vector<uint64_t> cum_w;  // cumulative owner-slice weights (empty: equal)
   // first element of owner slice q of a bucket of `units` 64-element units
-  size_t slice_at(size_t units, int q) const { return units * q / slice_nr * 64; }
+  size_t slice_at(size_t units, int q) const {
+    if (cum_w.empty()) return units * q / slice_nr * 64;
+    return (size_t)((unsigned __int128)units * cum_w[q] / cum_w[slice_nr]) * 64;
+  }
   bool has_bcast = false;
   FoldReq bcast;
   bool fused = false;                 // one fused kernel per bucket (RCV_FUSED)
@@ -2499,6 +2503,25 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
     p->has_comb = true;
     p->slice_q = d->slice_q;
     p->slice_nr = d->slice_nr;
+    if (d->slice_w) {
+      uint64_t acc = 0;
+      p->cum_w.push_back(0);
+      for (int q = 0; q < d->slice_nr; ++q) p->cum_w.push_back(acc += d->slice_w[q]);
+      if (acc == 0) {
+        delete p;
+        return set_err(RCV_EINVAL, "rcv_plan_create: owner-slice weights sum to 0");
+      }
+      // the combine's SM share follows this rank's slice (its loads and
+      // stores scale with the slice; the pre-reduce keeps the rest)
+      const double f = (double)d->slice_w[d->slice_q] / (double)acc * d->slice_nr;
+      const double share = std::min(0.7, std::max(0.1, comb_share(d) * f));
+      p->comb.max_ctas = getenv("RCV_COMB_CTAS") ? p->comb.max_ctas : std::max(1, (int)(share * ctx->sms));
+      const int pre_ctas = getenv("RCV_PRE_CTAS") ? -1 : std::max(1, (int)((1.0 - share) * ctx->sms));
+      if (pre_ctas > 0) {
+        for (auto &r : p->pre) r.max_ctas = pre_ctas;
+        p->forest.max_ctas = pre_ctas;
+      }
+    }
   }
   // fused kernel: every local node a full perfect subtree (a forest of at
   // most 8 roots over fp32 leaves), the combine a tree of at most 64 leaves

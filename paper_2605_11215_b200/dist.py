@@ -89,6 +89,66 @@ def owner_slice(n: int, q: int, nr: int, align: int = 64):
     return (min(n, units * q // nr * align), min(n, units * (q + 1) // nr * align))
 
 
+def slice_weights(local_nodes: Sequence[int], n_nodes: int, gain: float = 0.95,
+                  scale: int = 4096) -> Optional[List[int]]:
+    """Owner-slice weights that balance the combine's NVLink directions.
+
+    With owner q holding local_nodes[q] of the n_nodes cover nodes and a
+    share f_q of each bucket (in bucket units): ingress_q = 1 + f_q (n - l_q - 1)
+    (the other nodes' slices it reads, plus the other owners' slices stored
+    into its primary) and egress_q = l_q + f_q (N - 1 - l_q).  Returns integer
+    weights minimising max over q of max(ingress, egress), or None when
+    equal slices are within `gain` of that optimum (a perfect cover always
+    is).  Deterministic: every live rank derives the same weights."""
+    N = len(local_nodes)
+    if N < 2:
+        return None
+
+    def load(fs):
+        return max(max(1 + f * (n_nodes - l - 1), l + f * (N - 1 - l))
+                   for f, l in zip(fs, local_nodes))
+
+    def feasible(T):
+        los, his = [], []
+        for l in local_nodes:
+            lo, hi = 0.0, 1.0
+            a = n_nodes - l - 1
+            if a > 0:
+                hi = min(hi, (T - 1) / a)
+            elif T < 1:
+                return None
+            b = N - 1 - l
+            if b > 0:
+                hi = min(hi, (T - l) / b)
+            elif b < 0:
+                lo = max(lo, (l - T) / -b)
+            elif l > T:
+                return None
+            if lo > hi:
+                return None
+            los.append(lo)
+            his.append(hi)
+        if sum(los) > 1 or sum(his) < 1:
+            return None
+        rest = 1 - sum(los)
+        room = sum(h - lo for h, lo in zip(his, los)) or 1.0
+        return [lo + (h - lo) * rest / room for h, lo in zip(his, los)]
+
+    t_eq = load([1.0 / N] * N)
+    lo_t, hi_t = 0.0, t_eq
+    best = None
+    for _ in range(50):
+        mid = (lo_t + hi_t) / 2
+        fs = feasible(mid)
+        if fs is None:
+            lo_t = mid
+        else:
+            hi_t, best = mid, fs
+    if best is None or load(best) > gain * t_eq:
+        return None
+    return [max(1, int(round(f * scale))) for f in best]
+
+
 def plan_bucket(owner: Dict[int, int], n_leaves: int, live_ranks: Sequence[int],
                 pool_slots: int):
     """Host plan of one bucket commit, identical on every rank.
@@ -435,11 +495,18 @@ class DistributedGradientCommit(GradientCommit):
 
         def arr(ctype, xs):
             return (ctype * max(1, len(xs)))(*xs)
+        weights = None
+        if os.environ.get("RCV_SLICE_BALANCE", "1") not in ("", "0"):
+            per = {rk: 0 for rk in ranks}
+            for rk, _ in slot_of.values():
+                per[rk] += 1
+            weights = slice_weights([per[rk] for rk in ranks], len(cover))
         keep = dict(pre_blocks=arr(Block, pre_blocks), pre_counts=arr(ctypes.c_int, pre_counts),
                     pre_leaves=arr(ctypes.c_uint32, pre_leaves),
                     pre_out=arr(ctypes.c_void_p, pre_out), comb=arr(Block, comb),
                     comb_out=arr(ctypes.c_void_p, [self.grad_ptr[r] for r in prim]),
-                    bcast_out=arr(ctypes.c_void_p, [self.grads[r].data_ptr() for r in mine[1:]]))
+                    bcast_out=arr(ctypes.c_void_p, [self.grads[r].data_ptr() for r in mine[1:]]),
+                    slice_w=arr(ctypes.c_uint32, weights or []))
         d = _lib.PlanDesc(
             n_pre=len(pre_counts), pre_blocks=keep["pre_blocks"], pre_counts=keep["pre_counts"],
             pre_leaves=keep["pre_leaves"], pre_out=keep["pre_out"],
@@ -457,7 +524,8 @@ class DistributedGradientCommit(GradientCommit):
             guarded=int(self.real_kill),
             fused=int(part and fused_eligible(
                 cover, slot_of, leaves, ranks, b, self._code,
-                aligned=self.lmax % 4 == 0 and self.numel % 4 == 0)))
+                aligned=self.lmax % 4 == 0 and self.numel % 4 == 0)),
+            slice_w=keep["slice_w"] if weights else None)
         self.rt.set_plan(d, keep)
 
     def _reduce_bucket(self, k: int, leaves) -> int:

@@ -60,9 +60,13 @@ def _worker(rank, world, port, combine_variant, q, fused=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("combine_variant,fused", [(0, False), (2, False), (0, True)])
-def test_distributed_commit_bitwise(combine_variant, fused):
-    world = min(torch.cuda.device_count(), 4)
+@pytest.mark.parametrize("combine_variant,fused,world", [
+    (0, False, 4), (2, False, 4), (0, True, 4),
+    # two ranks: after replica 3 dies the cover is 4 + 2 nodes and the owner
+    # slices are link-balanced 3:1 (dist.slice_weights)
+    (0, False, 2)])
+def test_distributed_commit_bitwise(combine_variant, fused, world):
+    world = min(torch.cuda.device_count(), world)
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
