@@ -2513,7 +2513,8 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       }
       // the combine's SM share follows this rank's slice (its loads and
       // stores scale with the slice; the pre-reduce keeps the rest)
-      const double f = (double)d->slice_w[d->slice_q] / (double)acc * d->slice_nr;
+      const char *ss = getenv("RCV_SLICE_SHARE");
+      const double f = (ss && !atoi(ss)) ? 1.0 : (double)d->slice_w[d->slice_q] / (double)acc * d->slice_nr;
       const double share = std::min(0.7, std::max(0.1, comb_share(d) * f));
       p->comb.max_ctas = getenv("RCV_COMB_CTAS") ? p->comb.max_ctas : std::max(1, (int)(share * ctx->sms));
       const int pre_ctas = getenv("RCV_PRE_CTAS") ? -1 : std::max(1, (int)((1.0 - share) * ctx->sms));

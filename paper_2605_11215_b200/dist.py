@@ -99,7 +99,10 @@ def slice_weights(local_nodes: Sequence[int], n_nodes: int, gain: float = 0.95,
     into its primary) and egress_q = l_q + f_q (N - 1 - l_q).  Returns integer
     weights minimising max over q of max(ingress, egress), or None when
     equal slices are within `gain` of that optimum (a perfect cover always
-    is).  Deterministic: every live rank derives the same weights."""
+    is).  Deterministic: every live rank derives the same weights.
+    Opt-in (RCV_SLICE_BALANCE=1): at N=2 the balanced 3:1 split measured
+    slower than equal slices even with the combine's SM share scaled to the
+    slice — the combine's rate follows its SMs, not this link model."""
     N = len(local_nodes)
     if N < 2:
         return None
@@ -496,7 +499,8 @@ class DistributedGradientCommit(GradientCommit):
         def arr(ctype, xs):
             return (ctype * max(1, len(xs)))(*xs)
         weights = None
-        if os.environ.get("RCV_SLICE_BALANCE", "1") not in ("", "0"):
+        # opt-in: measured slower at N=2 (profiles/r1f/schedule_ab.txt 10.)
+        if os.environ.get("RCV_SLICE_BALANCE", "0") not in ("", "0"):
             per = {rk: 0 for rk in ranks}
             for rk, _ in slot_of.values():
                 per[rk] += 1

@@ -13,10 +13,11 @@ import torch
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 
-def _worker(rank, world, port, combine_variant, q, fused=False):
+def _worker(rank, world, port, combine_variant, q, fused=False, balance=False):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
-                      RCV_FUSED="1" if fused else "0")
+                      RCV_FUSED="1" if fused else "0",
+                      RCV_SLICE_BALANCE="1" if balance else "0")
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world,
                             device_id=torch.device("cuda", rank))
@@ -62,10 +63,11 @@ def _worker(rank, world, port, combine_variant, q, fused=False):
 
 @pytest.mark.parametrize("combine_variant,fused,world", [
     (0, False, 4), (2, False, 4), (0, True, 4),
-    # two ranks: after replica 3 dies the cover is 4 + 2 nodes and the owner
-    # slices are link-balanced 3:1 (dist.slice_weights)
+    # two ranks: after replica 3 dies the cover is 4 + 2 nodes and, opted
+    # in, the owner slices are link-balanced 3:1 (dist.slice_weights)
     (0, False, 2)])
 def test_distributed_commit_bitwise(combine_variant, fused, world):
+    balance = world == 2
     world = min(torch.cuda.device_count(), world)
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -73,7 +75,7 @@ def test_distributed_commit_bitwise(combine_variant, fused, world):
     s.close()
     ctx = torch.multiprocessing.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, combine_variant, q, fused))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, combine_variant, q, fused, balance))
              for r in range(world)]
     for p in procs:
         p.start()
