@@ -2394,7 +2394,9 @@ double comb_share(const rcv_plan_desc *d) {
   const bool perfect = d->n_comb > 0 && d->n_comb == d->slice_nr;
   const char *v = getenv("RCV_PERFECT_SHARE");
   const double f = v ? atof(v) : 0.25;
-  return perfect && f > 0 ? f : kCombShare;
+  if (perfect && f > 0) return f;
+  const char *fr = getenv("RCV_FRAG_SHARE");  // fragmented covers (experiments)
+  return fr && atof(fr) > 0 ? atof(fr) : kCombShare;
 }
 
 int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {

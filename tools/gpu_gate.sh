@@ -1,3 +1,4 @@
 #!/bin/bash
-# link-balanced owner slices at N=2 (degraded cover 4 + 2 nodes)
-bash tools/gpu_envab.sh 2 "RCV_SLICE_BALANCE=1" "RCV_SLICE_BALANCE=0" "RCV_SLICE_BALANCE=1 RCV_SLICE_SHARE=0" "RCV_SLICE_BALANCE=0"
+# combine SM share of fragmented covers (post-failure layouts)
+bash tools/gpu_envab.sh 4 "RCV_FRAG_SHARE=0.35" "RCV_FRAG_SHARE=0.5" "RCV_FRAG_SHARE=0.25"
+bash tools/gpu_envab.sh 2 "RCV_FRAG_SHARE=0.35" "RCV_FRAG_SHARE=0.5" "RCV_FRAG_SHARE=0.25"
