@@ -2219,14 +2219,13 @@ int preload_module_kernels() {
   if (count(&n, mod) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuModuleGetFunctionCount");
   std::vector<CUfunction> fs(n);
   if (n && enumerate(fs.data(), n, mod) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuModuleEnumerateFunctions");
-  // One shared-memory carveout for every kernel: the runtime runs DIRECT
-  // (register-only) and TMA (up to ~200 KB of smem) kernels concurrently on
-  // two streams, and an SM configured for a large L1 by a DIRECT CTA cannot
-  // take a TMA CTA until it drains (measured: a queued broadcast idling
-  // 70 us behind a combine).  DIRECT loads bypass L1 (no_allocate), so they
-  // lose nothing to the max-shared split.  RCV_CARVEOUT=-1 keeps the default.
+  // Optional shared-memory carveout for every kernel (RCV_CARVEOUT=0..100).
+  // Hypothesis tested: DIRECT CTAs (no smem) keep SMs in a large-L1 split
+  // that blocks concurrent TMA CTAs.  Max-shared measured slower (pre-reduce
+  // 44 -> 50 us, profiles/r1f/schedule_ab.txt 2.), so the default (-1)
+  // leaves the driver's choice.
   const char *cv = getenv("RCV_CARVEOUT");
-  const int carveout = cv ? atoi(cv) : 100;
+  const int carveout = cv ? atoi(cv) : -1;
   for (CUfunction f : fs) {
     if (load(f) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuFuncLoad");
     if (carveout >= 0 &&
