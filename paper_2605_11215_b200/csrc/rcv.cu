@@ -503,6 +503,42 @@ __global__ void __launch_bounds__(256)
   if constexpr (kGate) gate_done(p);
 }
 
+// DIRECT, two vectors per thread per iteration, for small perfect trees
+// (ProgFull<L>, L <= 3: the multi-GPU combine over one partial per rank):
+// every input of both vectors is loaded before the first add or store, so a
+// thread keeps 2 x 2^L 16-byte loads in flight across the NVLink round trip
+// instead of 2^L (the loop body's stores otherwise fence the next loads).
+template <typename P> struct FullTree { static constexpr int value = -1; };
+template <int L> struct FullTree<ProgFull<L>> { static constexpr int value = L; };
+
+template <typename Prog>
+__global__ void __launch_bounds__(256)
+    fold_direct_pair_kernel(const __grid_constant__ FoldParams p) {
+  constexpr int L = FullTree<Prog>::value;
+  constexpr int NIN = 1 << L;
+  if (p.guard && (*p.guard & p.guard_mask)) return;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long v = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+       v < p.nvec; v += 2 * stride) {
+    const unsigned long long w = v + stride;
+    const bool has_w = w < p.nvec;
+    float4 x[2][NIN];
+#pragma unroll
+    for (int i = 0; i < NIN; ++i) {
+      x[0][i] = ld_vec<float>(p.in[i] + v * 16ull, false);
+      x[1][i] = has_w ? ld_vec<float>(p.in[i] + w * 16ull, false) : vzero<float4>();
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (u == 1 && !has_w) break;
+      float4 r = ProgFull<L>::template node<L, 0, float4>([&](int i) { return x[u][i]; });
+      if (p.divisor != 0.0) r = vdiv(r, p.divisor);
+      const unsigned long long off = (u ? w : v) * 16ull;
+      for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + off, r);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // TMA variant: cp.async.bulk producer warp + 4 consumer warps
 
@@ -1085,6 +1121,7 @@ struct FoldReq {
   // halves the per-byte cost of a branchy evaluator's control flow
   bool wide32 = false;
   bool pdl = false;  // launch as a programmatic dependent (cudaLaunchKernelEx)
+  bool pair = false;  // DIRECT: two vectors per thread (small perfect trees, fp32)
   // flag gate of a single vector launch (FoldParams::gate_*), runtime only
   const unsigned long long *gate_flags = nullptr;
   unsigned long long gate_value = 0;
@@ -1233,6 +1270,15 @@ int launch_direct_p(const FoldReq &r, unsigned long long e0, unsigned long long 
     }
   }
   if (r.gate_mask) return set_err(RCV_EINVAL, "gated launch of a program without a gated kernel");
+  if constexpr (std::is_same<A, float>::value && FullTree<Prog>::value >= 0 &&
+                FullTree<Prog>::value <= 3) {
+    if (r.pair && !r.pdl) {
+      // the same (SM-share-capped) grid: twice the bytes in flight per SM
+      fold_direct_pair_kernel<Prog><<<(unsigned)blocks, 256, 0, st>>>(p);
+      CK(cudaGetLastError());
+      return RCV_OK;
+    }
+  }
   if (r.pdl) {
     CK(launch_pdl(fold_direct_kernel<A, Prog>, (unsigned)blocks, 256, 0, st, p));
     return RCV_OK;
@@ -2495,6 +2541,9 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       const char *w = getenv("RCV_WIDE_COMB");
       const int wide = w ? atoi(w) : 1;
       p->comb.wide32 = wide >= 2 || (wide == 1 && p->comb.full_L < 0);
+      // RCV_PAIR: two vectors per thread for the DIRECT perfect-tree combine
+      const char *pr = getenv("RCV_PAIR");
+      p->comb.pair = pr ? atoi(pr) != 0 : true;
     }
     if (d->guarded) {
       // the combine reads live peers' partials: skip it once one timed out
