@@ -43,6 +43,7 @@ per-index gradients resident in HBM).
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Callable, Dict, List, Optional, Tuple
@@ -161,7 +162,6 @@ class GradientCommit:
     def _reuse_committed(self) -> bool:
         """Whether a bucket committed earlier in the step over the same leaf
         index set may keep its outputs instead of being relaunched."""
-        import os
         return os.environ.get("RCV_REUSE", "1") not in ("", "0") and \
             not getattr(self, "real_kill", False)
 
