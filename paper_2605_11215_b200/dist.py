@@ -254,16 +254,26 @@ class DeadPeerDetector:
     timed out — the crash-stop detection of comm.py:129-172 driven by the
     hardware instead of the simulator.  Optionally re-forms the torch
     process group without the dead ranks (ncclCommShrink via
-    torch.distributed.shrink_group)."""
+    torch.distributed.shrink_group).
 
-    def __init__(self, engine: "DistributedGradientCommit", inner=None, shrink: bool = False):
+    per_bucket=True also polls before every bucket's collective
+    ("during_sync", the injection points of trainer.py:425), so a death is
+    detected one bucket after the barrier that timed out instead of at the
+    end of the cascade.  Each poll synchronises the device, which serialises
+    the bucket pipeline: it trades step time for detection latency."""
+
+    def __init__(self, engine: "DistributedGradientCommit", inner=None, shrink: bool = False,
+                 per_bucket: bool = False):
         self.engine, self.inner, self.shrink = engine, inner, shrink
+        self.per_bucket = per_bucket
         self.known = 0
         self.detections: List[dict] = []
 
     def fire(self, phase, bucket=None):
         out = list(self.inner.fire(phase, bucket)) if self.inner is not None else []
-        if phase not in ("after_sync", "before_sync"):
+        polls = ("after_sync", "before_sync", "during_sync") if self.per_bucket else \
+            ("after_sync", "before_sync")
+        if phase not in polls:
             return out
         import time
         t0 = time.perf_counter()
@@ -273,7 +283,7 @@ class DeadPeerDetector:
             self.known |= bits
             dead_ranks = [r for r in range(self.engine.world) if (bits >> r) & 1]
             victims = [rid for rid in self.engine.comm.members if self.engine.rank_of[rid] in dead_ranks]
-            rec = {"phase": phase, "ranks": dead_ranks, "replicas": victims,
+            rec = {"phase": phase, "bucket": bucket, "ranks": dead_ranks, "replicas": victims,
                    "sync_ms": (time.perf_counter() - t0) * 1e3}
             if self.shrink and hasattr(dist, "shrink_group"):
                 t1 = time.perf_counter()

@@ -16,7 +16,7 @@ import torch
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, per_bucket=False):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
@@ -34,7 +34,8 @@ def _worker(rank, world, port, q):
         dev = [torch.from_numpy(h).cuda() for h in host]
         want = fold.canonical_tree(dict(enumerate(host)), b) / np.float32(b)
         eng = DistributedGradientCommit(numel, w, g, 4, real_kill=True, barrier_timeout_s=1.0)
-        inj = RealKill(1, "during_sync", 2) if rank == 1 else DeadPeerDetector(eng, shrink=True)
+        inj = RealKill(1, "during_sync", 2) if rank == 1 else DeadPeerDetector(eng, shrink=True,
+                                                                              per_bucket=per_bucket)
         res = []
         for t in range(4):
             inj.step = t
@@ -54,7 +55,8 @@ def _worker(rank, world, port, q):
     os._exit(0)
 
 
-def test_real_process_death_recovered_in_step():
+@pytest.mark.parametrize("per_bucket", [False, True])
+def test_real_process_death_recovered_in_step(per_bucket):
     world = min(torch.cuda.device_count(), 4)
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -62,7 +64,7 @@ def test_real_process_death_recovered_in_step():
     s.close()
     ctx = torch.multiprocessing.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, per_bucket)) for r in range(world)]
     for p in procs:
         p.start()
     got = {}
@@ -81,4 +83,7 @@ def test_real_process_death_recovered_in_step():
         assert [wc for _, _, wc, _ in res] == [2 * world, 2 * world - 2, 2 * world - 2, 2 * world - 2]
         ev = res[1][3]
         assert len(ev) == 1 and ev[0]["failed"] == [2, 3] and ev[0]["at_boundary"]
-        assert det and det[0]["ranks"] == [1] and det[0]["phase"] == "after_sync"
+        assert det and det[0]["ranks"] == [1]
+        # per-bucket polling sees bucket 2's timed-out barrier before bucket 3
+        want_at = ("during_sync", 3) if per_bucket else ("after_sync", None)
+        assert (det[0]["phase"], det[0]["bucket"]) == want_at, det
