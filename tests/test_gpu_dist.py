@@ -282,9 +282,9 @@ def _eight_rank_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-# 1 of 11 runs on a 2-GPU box (4 ranks per GPU, time-sliced contexts) gave
+# 1 of 21 runs on 2-GPU boxes (4 ranks per GPU, time-sliced contexts) gave
 # wrong bits on rank 0's failure step (accounting exact; steps 0 and 2
-# bitwise); the other 10 passed with RCV_REUSE=1 and =0.  Open until the
+# bitwise, the first run on a fresh box); the other 20 passed (RCV_REUSE=1 and =0).  Open until the
 # race is found, so it does not gate the suite.
 @pytest.mark.xfail(strict=False, reason="rare mismatch on the failure step with shared GPUs")
 def test_eight_ranks_configs1_shape_shared_gpus():
