@@ -231,19 +231,27 @@ int rcv_barrier(uint64_t *local_flags, void *const *peer_flags, int n, int me,
  * One context per rank (flags, status, a side stream for pre-reduces, the
  * barrier sequence, the pending local broadcasts); one plan per leaf cover
  * (prepared fold requests: validated once, relaunched per bucket).  A bucket
- * then costs the host one call: rcv_plan_bucket enqueues
- *   side stream:  wait(pool set free) -> [broadcasts, fragmented covers] ->
- *                 pre-reduce nodes -> record(ready)
- *   main stream:  wait(ready) -> barrier -> record(arrived) -> combine(owner slice)
+ * call j then costs the host one call: rcv_plan_bucket enqueues
+ *   main stream:  [membership shrank since the previous call: barrier over
+ *                 the previous live mask, departing ranks included] ->
+ *   side stream:  wait(barrier j-2: pool set j%3 free) -> [broadcasts,
+ *                 fragmented covers] -> stamp(set) = 0 -> pre-reduce nodes
+ *                 into pool set j%3 -> stamp(set) = j+1 -> record(ready)
+ *   main stream:  wait(ready) -> barrier -> record(arrived) ->
+ *                 combine(owner slice; checks every producer's stamp == j+1
+ *                 before its first and after its last load)
  *   bcast stream: wait(arrived) -> broadcasts of the buckets combined before
  *                 (perfect covers: one node per live rank)
  * and rcv_ctx_finish closes the step (barrier + last broadcasts).
- * RCV_GATE=1 (opt-in) replaces the barrier by per-call ready/done flags the
- * combine kernel acquires/releases itself.  rcv_ctx_create loads every
- * kernel of the library up front (CUDA lazy loading could otherwise need a
- * context sync while a kernel waits on a peer's flag).
- * local_flags / peer_flags: 192 uint64 per rank ([0,64) barrier, [64,128)
- * fused kernel, [128,160) gate ready, [160,192) gate done). */
+ * rcv_ctx_create loads every kernel of the library up front (CUDA lazy
+ * loading could otherwise need a context sync while a kernel waits on a
+ * peer's flag).
+ * local_flags / peer_flags: 128 uint64 per rank ([0,64) barrier sequence per
+ * peer, [64,67) pool-set stamps).
+ * status: two uint32 words: [0] peers that timed out (bit per rank),
+ * [1] stamp mismatches seen by this rank's combines (bit 0: a partial was
+ * not ready, bit 1: it was overwritten while being read).  Nonzero word 1
+ * means the committed bits of that step are not trustworthy. */
 typedef struct rcv_ctx rcv_ctx;
 typedef struct rcv_plan rcv_plan;
 
@@ -255,7 +263,7 @@ int rcv_ctx_finish(rcv_ctx *ctx, uint64_t live_mask, int participate,
                    void *main_stream);
 int rcv_ctx_set_timing(rcv_ctx *ctx, int on);
 /* Drain recorded launch timings (call after synchronising): up to `max`
- * entries of kind (0 pre-reduce, 1 barrier, 2 broadcast, 3 combine, 4 fused),
+ * entries of kind (0 pre-reduce, 1 barrier, 2 broadcast, 3 combine),
  * milliseconds, algorithmic HBM bytes, NVLink in / out bytes. */
 int rcv_ctx_timing(rcv_ctx *ctx, int max, int *kind, float *ms, double *bytes,
                    double *nvl_in, double *nvl_out, int *count);
@@ -269,6 +277,7 @@ typedef struct {
   size_t set_stride;             /* elements from pool set 0 to set 1 */
   int n_comb;                    /* cover nodes (0: this rank takes no part) */
   const rcv_block *comb_blocks;  /* every node's pool slot in set 0, ascending lo */
+  const int *comb_rank;          /* rank producing each cover node (stamps) */
   uint32_t n_leaves;             /* B */
   int n_comb_out;
   void *const *comb_out;         /* primary replica of every live rank */
@@ -283,14 +292,7 @@ typedef struct {
   int participate;
   int remote_in, remote_out;     /* NVLink accounting of the combine */
   int guarded;                   /* real-kill mode: skip the combine once a
-                                    live peer timed out (status word) */
-  int fused;                     /* one fused pre-reduce+combine kernel per
-                                    bucket (every live rank must agree; needs
-                                    fp32, <= 8 perfect local nodes, <= 64
-                                    local leaves, n_leaves <= 64) */
-  const uint32_t *slice_w;       /* slice_nr owner-slice weights in slice
-                                    order (NULL: equal slices); every live
-                                    rank must pass the same weights */
+                                    live peer timed out (status word 0) */
 } rcv_plan_desc;
 
 int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *desc, rcv_plan **out);

@@ -53,6 +53,7 @@ class PlanDesc(ctypes.Structure):
         ("pre_leaves", ctypes.POINTER(ctypes.c_uint32)),
         ("pre_out", ctypes.POINTER(ctypes.c_void_p)), ("set_stride", ctypes.c_size_t),
         ("n_comb", ctypes.c_int), ("comb_blocks", ctypes.POINTER(_Block)),
+        ("comb_rank", ctypes.POINTER(ctypes.c_int)),
         ("n_leaves", ctypes.c_uint32), ("n_comb_out", ctypes.c_int),
         ("comb_out", ctypes.POINTER(ctypes.c_void_p)),
         ("slice_q", ctypes.c_int), ("slice_nr", ctypes.c_int),
@@ -62,8 +63,7 @@ class PlanDesc(ctypes.Structure):
         ("variant", ctypes.c_int), ("comb_variant", ctypes.c_int),
         ("live_mask", ctypes.c_uint64), ("participate", ctypes.c_int),
         ("remote_in", ctypes.c_int), ("remote_out", ctypes.c_int),
-        ("guarded", ctypes.c_int), ("fused", ctypes.c_int),
-        ("slice_w", ctypes.POINTER(ctypes.c_uint32)),
+        ("guarded", ctypes.c_int),
     ]
 
 
@@ -406,7 +406,7 @@ class TreePlan:
                        self.variant, stream))
 
 
-KIND_NAMES = ("prereduce", "barrier", "broadcast", "combine", "fused")
+KIND_NAMES = ("prereduce", "barrier", "broadcast", "combine")
 
 
 class BucketRuntime:

@@ -323,6 +323,7 @@ class GradientCommit:
             counts.append((rid, state.g_cur if role is ReplicaRole.MAJOR else (
                 state.r_cur if role is ReplicaRole.MINOR else 0)))
         ranges = self._canonical_ranges(counts)
+        cur_range = {r: list(v) for r, v in ranges.items()}
         majors = [r for r in comm.members if comm.roles[r] is ReplicaRole.MAJOR]
         minors = [r for r in comm.members if comm.roles[r] is ReplicaRole.MINOR]
         shadow: Dict[int, int] = {}
@@ -425,8 +426,10 @@ class GradientCommit:
             vacating = [r for r in sorted(rec.failed_replicas)
                         if roles_before.get(r) in SPARE_FOR]
             for (rid, new_role), dead in zip(rec.promotions, vacating):
-                got = [i for i in ranges.get(dead, [])]
-                admitted[rid].extend(got)
+                # the vacated replica's current range: a spare promoted
+                # earlier in this step holds the range it took over
+                cur_range[rid] = list(cur_range.get(dead, []))
+                admitted[rid].extend(cur_range[rid])
                 comm.contrib_regular[rid] += len(provisional[rid])
                 provisional[rid] = []
                 role_now[rid] = new_role

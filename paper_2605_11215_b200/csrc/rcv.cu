@@ -42,7 +42,7 @@
 
 #include "../../include/rcv.h"
 
-#define RCV_VERSION 1
+#define RCV_VERSION 2
 
 // ---------------------------------------------------------------------------
 // errors
@@ -265,88 +265,12 @@ struct FoldParams {
   // canonical tree (ProgTree): heap-indexed nodes, id = 2^(L-level)-1+idx
   int8_t node_in[2 * RCV_MAX_IN - 1];    // input feeding the node, or -1
   uint8_t present[2 * RCV_MAX_IN - 1];   // subtree holds at least one input
-  // flag gate (multi-process runtime, gate_mask != 0): before its first read
-  // every CTA waits until gate_flags[r] >= gate_value for each rank bit r
-  // (the producers' "partials ready" sequence, raised from peer GPUs), and
-  // the last CTA to finish releases done_value into every done_out[i] (the
-  // consumers' "this call's pool set is read and its slices are stored")
-  const unsigned long long *gate_flags;
-  unsigned long long gate_value;
-  unsigned int gate_mask;
-  unsigned int *gate_status;  // timeout / dead-peer bits (barrier status word)
-  unsigned long long gate_timeout_ns;
-  unsigned int *done_counter;  // device-local CTA count, reset by the last CTA
-  unsigned long long *done_out[32];
-  int n_done;
-  unsigned long long done_value;
-  // launched as a programmatic dependent (PDL) of the previous kernel in its
-  // stream: wait for that grid's completion and memory before any access
-  int pdl;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
-}
-
-// One thread waits until flags[r] >= value for every rank bit r of mask,
-// each wait bounded by %globaltimer.  A rank already marked in *status, or
-// one that times out (then marked), is not waited for; with `strict` the
-// call then returns false (the caller must not read that rank's memory).
-__device__ __noinline__ bool flag_wait(const unsigned long long *flags, unsigned long long value,
-                                       unsigned int mask, unsigned int *status,
-                                       unsigned long long timeout_ns, bool strict) {
-  bool ok = true;
-  for (int r = 0; r < 32; ++r) {
-    if (!((mask >> r) & 1u)) continue;
-    const unsigned long long t0 = globaltimer();
-    for (;;) {
-      unsigned long long v;
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + r) : "memory");
-      if (v >= value) break;
-      if (*(volatile unsigned int *)status & (1u << r)) {  // known dead
-        ok = !strict && ok;
-        break;
-      }
-      if (globaltimer() - t0 > timeout_ns) {
-        atomicOr(status, 1u << r);
-        ok = !strict && ok;
-        break;
-      }
-    }
-  }
-  return ok;
-}
-
-// Every thread of the CTA calls this before its first load of a gated launch:
-// thread 0 acquires the producers' ready flags; false when one of them is
-// dead or timed out (then nothing may be read, but gate_done still runs).
-__device__ __noinline__ bool gate_enter(const FoldParams &p) {
-  __shared__ int s_ok;
-  if (threadIdx.x == 0)
-    s_ok = !(p.guard && (*p.guard & p.guard_mask)) &&
-           flag_wait(p.gate_flags, p.gate_value, p.gate_mask, p.gate_status, p.gate_timeout_ns, true);
-  __syncthreads();
-  return s_ok != 0;
-}
-
-// Every thread of the CTA calls this after its last store of a gated launch:
-// the CTA's stores are made visible system-wide, counted, and the last CTA of
-// the grid releases the done sequence to every consumer rank.
-__device__ __noinline__ void gate_done(const FoldParams &p) {
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int prev = atomicAdd(p.done_counter, 1u);
-    if (prev + 1 == gridDim.x) {
-      atomicExch(p.done_counter, 0u);  // ready for the next gated launch
-      __threadfence_system();
-      for (int i = 0; i < p.n_done; ++i)
-        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.done_out[i]), "l"(p.done_value)
-                     : "memory");
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -477,21 +401,11 @@ __device__ __forceinline__ void emit(const FoldParams &p, const Ld &ld, unsigned
 // ---------------------------------------------------------------------------
 // DIRECT variant: 128-bit LDG straight from (local or peer) global memory
 
-template <typename A, typename Prog, bool kGate = false>
+template <typename A, typename Prog>
 __global__ void __launch_bounds__(256)
     fold_direct_kernel(const __grid_constant__ FoldParams p) {
   using V = typename VecT<A>::V;
-  if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
-  if constexpr (kGate) {
-    // the loads below are L1::no_allocate, so no line of a pool slot can be
-    // cached on this SM before its producer's ready flag was acquired
-    if (!gate_enter(p)) {
-      gate_done(p);
-      return;
-    }
-  } else if (p.guard && (*p.guard & p.guard_mask)) {
-    return;
-  }
+  if (p.guard && (*p.guard & p.guard_mask)) return;
   for (unsigned long long v = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
        v < p.nvec; v += (unsigned long long)gridDim.x * blockDim.x) {
     auto ld = [&](int i) {
@@ -500,7 +414,6 @@ __global__ void __launch_bounds__(256)
     };
     emit<Prog, V>(p, ld, v * (unsigned long long)VecT<A>::OUT);
   }
-  if constexpr (kGate) gate_done(p);
 }
 
 // DIRECT, two vectors per thread per iteration, for small perfect trees
@@ -584,20 +497,16 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src,
       : "memory");
 }
 
-template <typename A, typename Prog, bool kGate = false>
+template <typename A, typename Prog>
 __global__ void __launch_bounds__(TMA_THREADS)
     fold_tma_kernel(const __grid_constant__ FoldParams p) {
   using V = typename VecT<A>::V;
-  // returns at once unless the grid was launched as a PDL dependent
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  const bool guarded = p.guard && (*p.guard & p.guard_mask);
-  if (!kGate && guarded) return;  // uniform: before any barrier
+  if (p.guard && (*p.guard & p.guard_mask)) return;  // uniform: before any barrier
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)p.stages * p.stage_bytes);
   uint64_t *empty = full + p.stages;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  __shared__ int s_skip;
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
@@ -605,20 +514,11 @@ __global__ void __launch_bounds__(TMA_THREADS)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    // gated launch: this thread is also the TMA producer, so its acquire of
-    // the producers' ready flags, followed by a generic->async proxy fence,
-    // orders every bulk copy below after the peers' partial stores
-    s_skip = 0;
-    if constexpr (kGate) {
-      s_skip = guarded || !flag_wait(p.gate_flags, p.gate_value, p.gate_mask, p.gate_status,
-                                     p.gate_timeout_ns, true);
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
   }
   __syncthreads();
 
   const unsigned long long tv = (unsigned long long)TMA_CONSUMERS * p.vpt;
-  const unsigned long long ntiles = s_skip ? 0 : (p.nvec + tv - 1) / tv;
+  const unsigned long long ntiles = (p.nvec + tv - 1) / tv;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -643,7 +543,6 @@ __global__ void __launch_bounds__(TMA_THREADS)
         }
       }
     }
-    if constexpr (kGate) gate_done(p);
     return;
   }
 
@@ -671,7 +570,6 @@ __global__ void __launch_bounds__(TMA_THREADS)
       phase ^= 1;
     }
   }
-  if constexpr (kGate) gate_done(p);
 }
 
 // ---------------------------------------------------------------------------
@@ -864,20 +762,26 @@ struct BarrierParams {
   unsigned long long timeout_ns;
   int n;
   int me;
-  int fence;  // leading __threadfence_system (RCV_BAR_FENCE, default on)
+  // pool-set integrity stamps (multi-process runtime): after the wait, the
+  // stamps the next combine will read must equal now_value (bit 0 of *err
+  // otherwise: a partial is not ready), and the stamps the previous combine
+  // read must still equal prev_value (bit 1: a producer invalidated them,
+  // i.e. started overwriting a partial, before that combine had finished)
+  const unsigned long long *chk_now[32];
+  const unsigned long long *chk_prev[32];
+  int n_now, n_prev;
+  unsigned long long now_value, prev_value;
+  unsigned int *err;
 };
 
 __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   const int t = threadIdx.x;
-  // a PDL-launched combine behind this barrier may start its CTAs now; they
-  // block in griddepcontrol.wait until this grid has completed
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // a peer that already timed out is dead: never signal or wait on it again
   const unsigned int dead = *(volatile const unsigned int *)p.status;
   const bool peer = t < p.n && t != p.me && ((p.live >> t) & 1ull) && !((dead >> t) & 1u);
   // everything this GPU wrote before this kernel (partials, remote stores)
   // is made visible system-wide before the flag store releases it
-  if (p.fence) __threadfence_system();
+  __threadfence_system();
   if (peer)
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.peer[t] + p.me), "l"(p.value)
                  : "memory");
@@ -895,180 +799,16 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   }
   __syncthreads();
   __threadfence_system();
-}
-
-// Flag signal / wait of the gated runtime (RCV_GATE): release `signal_value`
-// into every signal[i] after a system fence (so everything this GPU wrote
-// before the launch is visible to the peers that acquire it), then wait until
-// wait_flags[r] >= wait_value for each rank bit of wait_mask.  Dead or
-// timed-out ranks are skipped and marked in the status word.
-struct GateParams {
-  unsigned long long *signal[32];
-  int n_signal;
-  unsigned long long signal_value;
-  const unsigned long long *wait_flags;
-  unsigned long long wait_value;
-  unsigned int wait_mask;
-  unsigned int *status;
-  unsigned long long timeout_ns;
-};
-
-__global__ void gate_kernel(const __grid_constant__ GateParams p) {
-  const int t = threadIdx.x;
-  if (p.n_signal) {
-    __threadfence_system();
-    if (t < p.n_signal)
-      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.signal[t]), "l"(p.signal_value)
-                   : "memory");
-  }
-  if (p.wait_mask && t == 0)
-    flag_wait(p.wait_flags, p.wait_value, p.wait_mask, p.status, p.timeout_ns, false);
-  __syncthreads();
-}
-
-// ---------------------------------------------------------------------------
-// fused bucket kernel (multi-process): local pre-reduce and the owner-slice
-// combine in ONE launch, synchronised per owner slice by release/acquire
-// flags in peer memory instead of a barrier kernel between two launches.
-//
-//   CTAs [0, a_ctas)   phase A: the rank's cover nodes (a forest of perfect
-//                      trees over its local leaves) into its pool slots,
-//                      slice by slice in owner order; the last CTA to finish
-//                      slice q releases `seq` into owner q's ready[me] flag.
-//   CTAs [a_ctas, ..)  phase B: acquire ready[p] >= seq from every producer
-//                      p (bounded by %globaltimer), then fold this rank's
-//                      slice over every node's partial (peers' over NVLink),
-//                      divide, and store it into every live rank's primary.
-//
-// Phase-A CTAs never wait and the grid never exceeds one CTA per SM, so all
-// CTAs are co-resident and the kernel cannot deadlock on its own GPU; a
-// producer that stops responding times out into the status word and the
-// combine is skipped (real-kill mode).
-
-#define FUSED_T 256
-#define FUSED_MAX_SLICES 32
-
-struct FusedParams {
-  // phase A
-  const char *leaf[RCV_MAX_IN];
-  int n_leaf;
-  int n_roots;
-  uint8_t root_L[8];
-  uint8_t root_first[8];
-  char *pool_out[8];
-  // phase B
-  const char *node[RCV_MAX_IN];
-  int n_node;
-  int8_t node_in[2 * RCV_MAX_IN - 1];
-  uint8_t present[2 * RCV_MAX_IN - 1];
-  char *out[FUSED_MAX_SLICES];
-  int n_out;
-  double divisor;
-  unsigned long long slice_lo[FUSED_MAX_SLICES + 1];  // in vectors
-  int n_slices;
-  int my_slice;
-  unsigned long long *ready_out[FUSED_MAX_SLICES];     // owner q's ready array
-  unsigned long long *ready_in;
-  unsigned int producers;  // rank bits this rank's combine waits for
-  unsigned int guard_mask;
-  int me;
-  unsigned long long seq;
-  unsigned int *counter;   // device-local, one per slice
-  unsigned int *status;
-  unsigned long long timeout_ns;
-  int a_ctas;
-  int tail;  // n mod 4 trailing elements, handled by scalar code
-};
-
-// coherent 16-byte load (the pool slot was written during this kernel, on
-// this or another GPU): bypass L1, no read-only path
-__device__ __forceinline__ float4 ld_cg_f4(const char *p) {
-  float4 v;
-  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p)
-               : "memory");
-  return v;
-}
-
-template <typename ProgB>
-__global__ void __launch_bounds__(FUSED_T, 4)
-    fused_bucket_kernel(const __grid_constant__ FusedParams p) {
-  const int tid = threadIdx.x;
-  if ((int)blockIdx.x < p.a_ctas) {
-    // ---- phase A: local partials, slice by slice in owner order ----
-    const int a = blockIdx.x;
-    for (int q = 0; q < p.n_slices; ++q) {
-      for (unsigned long long v = p.slice_lo[q] + (unsigned long long)a * FUSED_T + tid;
-           v < p.slice_lo[q + 1]; v += (unsigned long long)p.a_ctas * FUSED_T) {
-        auto ld = [&](int i) { return ld_vec<float>(p.leaf[i] + v * 16ull, false); };
-        ProgForest::run<float4>(p, ld, [&](int f, float4 r) { st_vec(p.pool_out[f] + v * 16ull, r); });
-      }
-      if (q == p.n_slices - 1 && a == 0 && tid < p.tail) {  // ragged end: scalar
-        const unsigned long long e = p.slice_lo[p.n_slices] * 4ull + tid;
-        auto ld = [&](int i) { return reinterpret_cast<const float *>(p.leaf[i])[e]; };
-        ProgForest::run<float>(p, ld, [&](int f, float r) {
-          reinterpret_cast<float *>(p.pool_out[f])[e] = r;
-        });
-      }
-      __threadfence_system();  // this thread's partial stores, before the count
-      __syncthreads();
-      if (tid == 0) {
-        const unsigned int done = atomicAdd(&p.counter[q], 1u) + 1u;
-        if (done == (unsigned int)p.a_ctas) {  // the slice is complete here
-          p.counter[q] = 0u;                   // ready for the next call
-          __threadfence_system();
-          asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.ready_out[q] + p.me),
-                       "l"(p.seq)
-                       : "memory");
-        }
-      }
+  if (t < p.n_prev || t < p.n_now) {
+    unsigned long long v;
+    if (t < p.n_prev) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.chk_prev[t]) : "memory");
+      if (v != p.prev_value) atomicOr(p.err, 2u);
     }
-    return;
-  }
-  // ---- phase B: this rank's slice, once every producer's partial is in ----
-  if (p.my_slice < 0) return;
-  __shared__ int skip;
-  if (tid == 0) {
-    skip = 0;
-    for (int r = 0; r < 32; ++r) {
-      if (!((p.producers >> r) & 1u)) continue;
-      const unsigned long long t0 = globaltimer();
-      unsigned long long v;
-      for (;;) {
-        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.ready_in + r) : "memory");
-        if (v >= p.seq) break;
-        if (*(volatile unsigned int *)p.status & p.guard_mask & (1u << r)) {  // known dead
-          skip = 1;
-          break;
-        }
-        if (globaltimer() - t0 > p.timeout_ns) {
-          atomicOr(p.status, 1u << r);
-          skip = 1;
-          break;
-        }
-      }
+    if (t < p.n_now) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.chk_now[t]) : "memory");
+      if (v != p.now_value) atomicOr(p.err, 1u);
     }
-  }
-  __syncthreads();
-  if (skip) return;
-  const int b = blockIdx.x - p.a_ctas;
-  const int nb = gridDim.x - p.a_ctas;
-  const int q = p.my_slice;
-  for (unsigned long long v = p.slice_lo[q] + (unsigned long long)b * FUSED_T + tid;
-       v < p.slice_lo[q + 1]; v += (unsigned long long)nb * FUSED_T) {
-    auto ld = [&](int i) { return ld_cg_f4(p.node[i] + v * 16ull); };
-    float4 r = ProgB::template eval<float4>(p, ld);
-    if (p.divisor != 0.0) r = vdiv(r, p.divisor);
-    for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + v * 16ull, r);
-  }
-  // the bucket's ragged end (n mod 4 elements) belongs to the last slice
-  if (q == p.n_slices - 1 && b == 0 && tid < p.tail) {
-    const unsigned long long e = p.slice_lo[p.n_slices] * 4ull + tid;
-    auto ld = [&](int i) { return __ldcg(reinterpret_cast<const float *>(p.node[i]) + e); };
-    float r = ProgB::template eval<float>(p, ld);
-    if (p.divisor != 0.0) r = __fdiv_rn(r, (float)p.divisor);
-    for (int j = 0; j < p.n_out; ++j) reinterpret_cast<float *>(p.out[j])[e] = r;
   }
 }
 
@@ -1120,18 +860,7 @@ struct FoldReq {
   // fp32 inputs evaluated as 8-element vectors (two 16-byte loads per input):
   // halves the per-byte cost of a branchy evaluator's control flow
   bool wide32 = false;
-  bool pdl = false;  // launch as a programmatic dependent (cudaLaunchKernelEx)
   bool pair = false;  // DIRECT: two vectors per thread (small perfect trees, fp32)
-  // flag gate of a single vector launch (FoldParams::gate_*), runtime only
-  const unsigned long long *gate_flags = nullptr;
-  unsigned long long gate_value = 0;
-  unsigned int gate_mask = 0;
-  unsigned int *gate_status = nullptr;
-  unsigned long long gate_timeout_ns = 0;
-  unsigned int *done_counter = nullptr;
-  unsigned long long *done_out[32];
-  int n_done = 0;
-  unsigned long long done_value = 0;
 };
 
 enum { PK_STACK = 0, PK_LEFT = 1, PK_TREE = 2 };
@@ -1210,16 +939,6 @@ void fill_vec_params(FoldParams &p, const FoldReq &r, unsigned long long e0,
   p.guard = r.guard;
   p.guard_mask = r.guard_mask;
   p.n_roots = r.n_roots;
-  p.pdl = r.pdl;
-  p.gate_flags = r.gate_flags;
-  p.gate_value = r.gate_value;
-  p.gate_mask = r.gate_mask;
-  p.gate_status = r.gate_status;
-  p.gate_timeout_ns = r.gate_timeout_ns;
-  p.done_counter = r.done_counter;
-  for (int i = 0; i < r.n_done; ++i) p.done_out[i] = r.done_out[i];
-  p.n_done = r.n_done;
-  p.done_value = r.done_value;
   memcpy(p.root_L, r.root_L, sizeof p.root_L);
   memcpy(p.root_first, r.root_first, sizeof p.root_first);
   if (r.tree_L >= 0) {
@@ -1228,30 +947,6 @@ void fill_vec_params(FoldParams &p, const FoldReq &r, unsigned long long e0,
     memcpy(p.present, r.present, nodes);
   }
 }
-
-// Launch as a programmatic dependent of the previous kernel in `st` (PDL):
-// the grid may be scheduled while that kernel still runs and waits for it
-// in griddepcontrol.wait (FoldParams::pdl).
-cudaError_t launch_pdl(void (*kern)(FoldParams), unsigned blocks, unsigned threads, size_t smem,
-                       cudaStream_t st, const FoldParams &p) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, p);
-}
-
-// gated instantiations exist only for the combine's programs over fp32
-// pool slots (canonical trees of at most 64 leaves)
-template <typename A, typename Prog> struct Gatable { static constexpr bool value = false; };
-template <int L> struct Gatable<float, ProgTree<L>> { static constexpr bool value = true; };
-template <int L> struct Gatable<float, ProgFull<L>> { static constexpr bool value = true; };
 
 template <typename A, typename Prog>
 int launch_direct_p(const FoldReq &r, unsigned long long e0, unsigned long long nvec,
@@ -1262,26 +957,14 @@ int launch_direct_p(const FoldReq &r, unsigned long long e0, unsigned long long 
   unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)sms * 8));
   if (r.max_ctas > 0) blocks = std::min<unsigned long long>(blocks, (unsigned long long)r.max_ctas * 4);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  if constexpr (Gatable<A, Prog>::value) {
-    if (r.gate_mask) {
-      fold_direct_kernel<A, Prog, true><<<(unsigned)blocks, 256, 0, st>>>(p);
-      CK(cudaGetLastError());
-      return RCV_OK;
-    }
-  }
-  if (r.gate_mask) return set_err(RCV_EINVAL, "gated launch of a program without a gated kernel");
   if constexpr (std::is_same<A, float>::value && FullTree<Prog>::value >= 0 &&
                 FullTree<Prog>::value <= 3) {
-    if (r.pair && !r.pdl) {
+    if (r.pair) {
       // the same (SM-share-capped) grid: twice the bytes in flight per SM
       fold_direct_pair_kernel<Prog><<<(unsigned)blocks, 256, 0, st>>>(p);
       CK(cudaGetLastError());
       return RCV_OK;
     }
-  }
-  if (r.pdl) {
-    CK(launch_pdl(fold_direct_kernel<A, Prog>, (unsigned)blocks, 256, 0, st, p));
-    return RCV_OK;
   }
   fold_direct_kernel<A, Prog><<<(unsigned)blocks, 256, 0, st>>>(p);
   CK(cudaGetLastError());
@@ -1332,11 +1015,6 @@ int launch_tma_p(const FoldReq &r, const TmaGeom &g, unsigned long long e0,
   p.stages = g.stages;
   p.vpt = g.vpt;
   auto kern = fold_tma_kernel<A, Prog>;
-  if constexpr (Gatable<A, Prog>::value) {
-    if (r.gate_mask) kern = fold_tma_kernel<A, Prog, true>;
-  }
-  if (r.gate_mask && kern == fold_tma_kernel<A, Prog>)
-    return set_err(RCV_EINVAL, "gated launch of a program without a gated kernel");
   {
     // one attribute call per (kernel, device, size): it is not free
     static std::mutex mu;
@@ -1358,10 +1036,6 @@ int launch_tma_p(const FoldReq &r, const TmaGeom &g, unsigned long long e0,
       1, std::min<unsigned long long>(ntiles, (unsigned long long)sms * g.ctas_per_sm));
   if (r.max_ctas > 0) blocks = std::min<unsigned long long>(blocks, (unsigned long long)r.max_ctas);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (r.pdl) {
-    CK(launch_pdl(kern, (unsigned)blocks, TMA_THREADS, g.smem, st, p));
-    return RCV_OK;
-  }
   kern<<<(unsigned)blocks, TMA_THREADS, g.smem, st>>>(p);
   CK(cudaGetLastError());
   return RCV_OK;
@@ -1385,8 +1059,7 @@ int launch_vec(const FoldReq &r, bool tma, const TmaGeom &g, int maxd,
       default: RCV_LAUNCH(ProgFull<6>);
     }
   }
-  static const bool tree_as_stack = getenv("RCV_TREE_EVAL") && atoi(getenv("RCV_TREE_EVAL")) == 1;
-  if (r.tree_L >= 0 && r.tree_L <= 6 && !(tree_as_stack && maxd <= 8)) {
+  if (r.tree_L >= 0 && r.tree_L <= 6) {
     switch (r.tree_L) {
       case 0: RCV_LAUNCH(ProgTree<0>);
       case 1: RCV_LAUNCH(ProgTree<1>);
@@ -1472,27 +1145,6 @@ int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int s
     if (rc) return rc;
   }
   return RCV_OK;
-}
-
-// Whether run_fold issues exactly one vector launch for r over numel
-// elements (no scalar head or tail): the condition for a flag-gated launch.
-bool single_vec_launch(const FoldReq &r, size_t numel) {
-  if (numel == 0 || r.n_in == 0 || r.n_out == 0 || r.n_roots > 0) return false;
-  if (r.acc_dt != RCV_F32 || r.tree_L < 0 || r.tree_L > 6 || r.wide32) return false;  // Gatable programs
-  if (getenv("RCV_TREE_EVAL") && atoi(getenv("RCV_TREE_EVAL")) == 1) return false;
-  for (int i = 0; i < r.n_in; ++i)
-    if (r.in_dt[i] != RCV_F32) return false;
-  return common_head(r) == 0 && numel % 8 == 0;
-}
-
-// run_fold issues exactly one vector launch (any program, any dtype)
-bool single_vec_launch_any(const FoldReq &r, size_t numel) {
-  if (numel == 0 || r.n_in == 0 || r.n_out == 0) return false;
-  const bool f64 = r.acc_dt == RCV_F64;
-  bool wide = r.wide32 && !f64;
-  for (int i = 0; i < r.n_in && !f64; ++i) wide |= r.in_dt[i] == RCV_BF16;
-  const size_t E = f64 ? 2 : (wide ? 8 : 4);
-  return common_head(r) == 0 && numel % (2 * E) == 0;
 }
 
 int check_dtype(int acc_dt, int in_dt) {
@@ -1984,7 +1636,6 @@ int rcv_barrier(uint64_t *local_flags, void *const *peer_flags, int n, int me,
   p.timeout_ns = timeout_ns;
   p.n = n;
   p.me = me;
-  p.fence = 1;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
   CK(cudaGetLastError());
@@ -2069,11 +1720,25 @@ int rcv_toy_grad(int kind_linear, const double *params, const double *lanes,
   return RCV_OK;
 }
 
+}  // extern "C"
 
 // ---------------------------------------------------------------------------
 // native per-bucket runtime (multi-process commit)
 
-}  // extern "C"
+namespace {
+
+// pool-set integrity stamps live in the rank's flag array after the barrier
+// slots: word kStampBase + s belongs to pool set s (three sets)
+constexpr int kStampBase = 64;
+
+__global__ void stamp_kernel(unsigned long long *addr, unsigned long long value) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(addr), "l"(value) : "memory");
+}
+
+typedef CUresult (*WriteValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+
+}  // namespace
 
 struct TimingRec {
   int kind;
@@ -2084,36 +1749,30 @@ struct TimingRec {
 struct rcv_ctx {
   int n_ranks = 0, me = 0, device = 0, sms = 148;
   BarrierParams bar;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_main = nullptr, ev_ready = nullptr, ev_arrived[3] = {nullptr, nullptr, nullptr};
+  unsigned int *err = nullptr;  // status word 1: stamp mismatches seen by this rank's combines
+  cudaStream_t side = nullptr;     // pre-reduces (and fragmented covers' broadcasts)
+  cudaStream_t bstream = nullptr;  // perfect covers' broadcasts, right behind each barrier
+  cudaEvent_t ev_main = nullptr, ev_ready = nullptr, ev_trans = nullptr, ev_bcast = nullptr;
+  cudaEvent_t ev_arrived[3] = {nullptr, nullptr, nullptr};
   bool in_step = false;
+  bool bstream_dirty = false;  // bstream holds broadcasts the side stream has not waited for
   unsigned long long calls = 0, seq = 0;
+  // live mask of the previous bucket call in this step (0: none since the
+  // last rcv_ctx_finish).  A call whose mask drops ranks first joins one
+  // barrier over this mask, departing ranks included: their last combine
+  // read this rank's pool sets and stored into its primary.
+  uint64_t last_live = 0;
+  WriteValue64 write_value = nullptr;  // cuStreamWriteValue64 (stamp_kernel when absent)
+  // the stamps the last combine on main read, re-checked by the next barrier
+  std::vector<const unsigned long long *> chk;
+  unsigned long long chk_value = 0;
   struct Pending {
     FoldReq req;
     size_t lo, n;
     int variant;
     unsigned long long call;  // bucket call index that combined it
-    bool fused = false;       // combined by the fused kernel: complete only after a barrier
-    // copy-engine all-gather (RCV_CE_GATHER): pull each peer's finished
-    // slice of this bucket from its primary into ours before broadcasting
-    std::vector<std::pair<const char *, std::pair<size_t, size_t>>> gather;  // src base, [a, z)
-    char *dst = nullptr;
-    int es = 4;
   };
   std::vector<Pending> pending;  // combined buckets awaiting the local broadcast
-  // gated runtime (RCV_GATE, default on): per-call ready / done sequences in
-  // the flag arrays instead of a barrier kernel between pre-reduce and combine
-  bool gate = false;
-  // local broadcasts on their own stream, right behind each barrier
-  // (RCV_BCAST_STREAM), instead of between pre-reduces on the side stream
-  bool pdl = false;  // combine launched as a PDL dependent of its barrier (RCV_PDL=1)
-  cudaStream_t bstream = nullptr;
-  cudaEvent_t ev_bcast = nullptr;  // bstream's tail, for a side-stream flush after it
-  bool bstream_dirty = false;      // bstream holds broadcasts the side has not waited for
-  unsigned int *d_gate_counter = nullptr;  // CTAs of the running gated combine
-  unsigned int *d_counter = nullptr;  // fused kernel: phase-A CTAs done per slice
-  unsigned long long fseq = 0;        // fused kernel: ready-flag sequence
-  bool fused_in_step = false;
   bool timing = false;
   std::vector<TimingRec> recs;
   std::vector<cudaEvent_t> spare_events;
@@ -2127,6 +1786,7 @@ struct rcv_ctx {
     cudaEventCreate(&e);
     return e;
   }
+  unsigned long long *stamp_of(int rank, int set) const { return bar.peer[rank] + kStampBase + set; }
 };
 
 struct rcv_plan {
@@ -2140,26 +1800,16 @@ struct rcv_plan {
   bool has_comb = false;
   FoldReq comb;
   int slice_q = 0, slice_nr = 1;
-  std::vector<uint64_t> cum_w;  // cumulative owner-slice weights (empty: equal)
-  // first element of owner slice q of a bucket of `units` 64-element units
-  size_t slice_at(size_t units, int q) const {
-    if (cum_w.empty()) return units * q / slice_nr * 64;
-    return (size_t)((unsigned __int128)units * cum_w[q] / cum_w[slice_nr]) * 64;
-  }
+  std::vector<int> producers;  // distinct ranks whose pool slots the combine reads
   bool has_bcast = false;
   FoldReq bcast;
-  bool fused = false;                 // one fused kernel per bucket (RCV_FUSED)
-  FusedParams ftmpl;
-  void (*fkern)(FusedParams) = nullptr;
-  int fgrid = 0;
-  bool ce_gather = false;             // all-gather by copy engine instead of STG
-  std::vector<const char *> peer_primary;  // per live rank (slice order)
-  char *my_primary = nullptr;
   int variant = 0, comb_variant = 0;
   uint64_t live_mask = 0;
   bool participate = false;
   bool perfect = false;  // one cover node per live rank (the failure-free layout)
   int remote_in = 0, remote_out = 0;
+  // first element of owner slice q of a bucket of `units` 64-element units
+  size_t slice_at(size_t units, int q) const { return units * q / slice_nr * 64; }
 };
 
 namespace {
@@ -2175,10 +1825,31 @@ int timed(rcv_ctx *c, cudaStream_t st, int kind, double bytes, double nin, doubl
   return rc;
 }
 
-int ctx_barrier(rcv_ctx *c, uint64_t live, bool participate, cudaStream_t st) {
-  if (!participate || __builtin_popcountll(live) < 2) return RCV_OK;
+// `now`: the stamps the combine launched right behind this barrier reads
+// (checked == now_value after the wait); the previous combine's stamps are
+// re-checked by the same launch (BarrierParams::chk_*).
+int ctx_barrier(rcv_ctx *c, uint64_t live, bool participate, cudaStream_t st,
+                const std::vector<const unsigned long long *> *now = nullptr,
+                unsigned long long now_value = 0) {
+  if (!participate || __builtin_popcountll(live) < 2) {
+    c->chk.clear();  // no peer: nothing can race this rank's combines
+    return RCV_OK;
+  }
   c->bar.live = live;
   c->bar.value = ++c->seq;
+  c->bar.err = c->err;
+  c->bar.n_prev = (int)c->chk.size();
+  for (int i = 0; i < c->bar.n_prev; ++i) c->bar.chk_prev[i] = c->chk[i];
+  c->bar.prev_value = c->chk_value;
+  c->bar.n_now = now ? (int)now->size() : 0;
+  for (int i = 0; i < c->bar.n_now; ++i) c->bar.chk_now[i] = (*now)[i];
+  c->bar.now_value = now_value;
+  if (now) {
+    c->chk = *now;
+    c->chk_value = now_value;
+  } else {
+    c->chk.clear();
+  }
   return timed(c, st, 1, 0, 0, 0, [&]() {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     barrier_kernel<<<1, 32, 0, st>>>(c->bar);
@@ -2187,22 +1858,42 @@ int ctx_barrier(rcv_ctx *c, uint64_t live, bool participate, cudaStream_t st) {
   });
 }
 
+// Membership shrank since the previous call of this step: every rank of the
+// previous mask joins one barrier over it on its main stream, after its last
+// combine.  Passing it proves that the departing ranks' combines, which read
+// this rank's pool sets and stored into its primary replica, are complete,
+// so no pool set is rewritten and no bucket broadcast before they land.
+int ctx_transition(rcv_ctx *c, uint64_t live, cudaStream_t main) {
+  const uint64_t prev = c->last_live;
+  c->last_live = live;
+  if (!prev || !(prev & ~live)) return RCV_OK;
+  int rc = ctx_barrier(c, prev, (prev >> c->me) & 1ull, main);
+  if (rc) return rc;
+  CK(cudaEventRecord(c->ev_trans, main));
+  CK(cudaStreamWaitEvent(c->side, c->ev_trans, 0));
+  if (c->bstream) CK(cudaStreamWaitEvent(c->bstream, c->ev_trans, 0));
+  return RCV_OK;
+}
+
+int stamp_write(rcv_ctx *c, cudaStream_t st, unsigned long long *addr, unsigned long long v) {
+  if (c->write_value) {
+    // default flags: the write is preceded by a system-scope memory barrier
+    if (c->write_value((CUstream)st, (CUdeviceptr)addr, (cuuint64_t)v, 0) != CUDA_SUCCESS)
+      return set_err(RCV_ECUDA, "cuStreamWriteValue64");
+    return RCV_OK;
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  stamp_kernel<<<1, 1, 0, st>>>(addr, v);
+  CK(cudaGetLastError());
+  return RCV_OK;
+}
+
 // Broadcast the pending buckets combined at call index <= upto (all of them
 // when upto < 0) from this rank's primary replica to its other replicas.
 int ctx_flush(rcv_ctx *c, cudaStream_t st, long long upto) {
   while (!c->pending.empty() && (upto < 0 || (long long)c->pending.front().call <= upto)) {
-    // buckets committed by the fused kernel have no per-bucket barrier: only
-    // the step's closing barrier (upto < 0) proves their slices landed
-    if (upto >= 0 && c->pending.front().fused) break;
     rcv_ctx::Pending e = c->pending.front();
     c->pending.erase(c->pending.begin());
-    for (auto &g : e.gather) {
-      const size_t a = g.second.first, z = g.second.second;
-      if (z > a)
-        CK(cudaMemcpyAsync(e.dst + (e.lo + a) * e.es, g.first + (e.lo + a) * e.es,
-                           (z - a) * e.es, cudaMemcpyDeviceToDevice, st));
-    }
-    if (e.req.n_out == 0) continue;  // gather only: no other local replica
     shift(e.req, e.lo, e.lo);
     const double bytes = (double)(e.req.n_in + e.req.n_out) * e.n * esize(e.req.acc_dt);
     int rc = timed(c, st, 2, bytes, 0, 0,
@@ -2212,20 +1903,12 @@ int ctx_flush(rcv_ctx *c, cudaStream_t st, long long upto) {
   return RCV_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-}  // extern "C"
-
-namespace {
-
 // Load every kernel of this library's module on the current device.  Under
 // CUDA lazy loading (the default) the first launch of a kernel may need a
-// context synchronisation; if a flag-gated combine is already spinning for a
-// signal that kernel is to produce, that is a deadlock (broken only by the
-// wait's timeout).  So the runtime loads all of its kernels up front, once
-// per device, before any gated launch.
+// context synchronisation; if a barrier kernel is already spinning for a
+// signal a peer's not-yet-loaded kernel is to produce, that is a deadlock
+// (broken only by the wait's timeout).  So the runtime loads all of its
+// kernels up front, once per device.
 int preload_module_kernels() {
   static std::mutex mu;
   static std::vector<int> done;
@@ -2238,9 +1921,7 @@ int preload_module_kernels() {
   typedef CUresult (*Count)(unsigned int *, CUmodule);
   typedef CUresult (*Enum)(CUfunction *, unsigned int, CUmodule);
   typedef CUresult (*Load)(CUfunction);
-  typedef CUresult (*SetAttr)(CUfunction, CUfunction_attribute, int);
   GetModule get_module = nullptr;
-  SetAttr set_attr = nullptr;
   Count count = nullptr;
   Enum enumerate = nullptr;
   Load load = nullptr;
@@ -2250,36 +1931,45 @@ int preload_module_kernels() {
   } eps[] = {{"cuFuncGetModule", (void **)&get_module},
              {"cuModuleGetFunctionCount", (void **)&count},
              {"cuModuleEnumerateFunctions", (void **)&enumerate},
-             {"cuFuncLoad", (void **)&load},
-             {"cuFuncSetAttribute", (void **)&set_attr}};
+             {"cuFuncLoad", (void **)&load}};
   for (auto &e : eps) {
     cudaDriverEntryPointQueryResult q;
     CK(cudaGetDriverEntryPoint(e.name, e.fn, cudaEnableDefault, &q));
     if (q != cudaDriverEntryPointSuccess || !*e.fn) return set_err(RCV_ECUDA, "%s unavailable", e.name);
   }
   cudaFunction_t f0 = nullptr;
-  CK(cudaGetFuncBySymbol(&f0, (const void *)gate_kernel));
+  CK(cudaGetFuncBySymbol(&f0, (const void *)barrier_kernel));
   CUmodule mod = nullptr;
   if (get_module(&mod, (CUfunction)f0) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuFuncGetModule");
   unsigned int n = 0;
   if (count(&n, mod) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuModuleGetFunctionCount");
   std::vector<CUfunction> fs(n);
   if (n && enumerate(fs.data(), n, mod) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuModuleEnumerateFunctions");
-  // Optional shared-memory carveout for every kernel (RCV_CARVEOUT=0..100).
-  // Hypothesis tested: DIRECT CTAs (no smem) keep SMs in a large-L1 split
-  // that blocks concurrent TMA CTAs.  Max-shared measured slower (pre-reduce
-  // 44 -> 50 us, profiles/r1f/schedule_ab.txt 2.), so the default (-1)
-  // leaves the driver's choice.
-  const char *cv = getenv("RCV_CARVEOUT");
-  const int carveout = cv ? atoi(cv) : -1;
-  for (CUfunction f : fs) {
+  for (CUfunction f : fs)
     if (load(f) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuFuncLoad");
-    if (carveout >= 0 &&
-        set_attr(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, carveout) != CUDA_SUCCESS)
-      return set_err(RCV_ECUDA, "cuFuncSetAttribute(carveout)");
-  }
   done.push_back(dev);
   return RCV_OK;
+}
+
+// SM shares of the two concurrent streams (profiles/r1/caps_sweep.txt): the
+// NVLink-bound combine saturates the links with about a third of the SMs,
+// and a full-occupancy grid of either kernel would keep the other off the
+// GPU until its last wave drains.  Fragmented covers: combine 0.35 /
+// pre-reduce 0.65.  A perfect cover (one node per live rank, the
+// failure-free layout) moves the fewest NVLink bytes per HBM byte of
+// pre-reduce, so the pre-reduce sets the cadence and gets 0.75
+// (profiles/r1f/schedule_ab.txt).  RCV_COMB_CTAS / RCV_PRE_CTAS override
+// (an absolute CTA count > 2, or a fraction of the SMs; 0: uncapped).
+int env_ctas(const char *name, int sms, double dflt_frac) {
+  const char *v = getenv(name);
+  const double f = v ? atof(v) : dflt_frac;
+  if (f <= 0) return 0;
+  if (f > 2.0) return (int)f;
+  return std::max(1, (int)(f * sms));
+}
+
+double comb_share(const rcv_plan_desc *d) {
+  return d->n_comb > 0 && d->n_comb == d->slice_nr ? 0.25 : 0.35;
 }
 
 }  // namespace
@@ -2306,41 +1996,27 @@ int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer
   c->bar.timeout_ns = timeout_ns;
   c->bar.n = n_ranks;
   c->bar.me = me;
+  c->err = status + 1;
   {
-    const char *bf = getenv("RCV_BAR_FENCE");
-    c->bar.fence = bf ? atoi(bf) : 1;
+    // stream memory operations write the stamps without a kernel launch
+    int ok = 0;
+    cudaDeviceGetAttribute(&ok, (cudaDeviceAttr)CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, c->device);
+    cudaGetLastError();
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    if (ok && !getenv("RCV_STAMP_KERNEL") &&
+        cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && fn)
+      c->write_value = (WriteValue64)fn;
+    cudaGetLastError();
   }
-  // the side stream carries the HBM-bound critical path (pre-reduce and
-  // local broadcast); RCV_SIDE_PRIORITY=1 schedules its CTAs ahead of the
-  // NVLink-bound combine on the caller's stream
-  int lo_pri = 0, hi_pri = 0;
-  CK(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
-  const char *sp = getenv("RCV_SIDE_PRIORITY");
-  CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking,
-                                  (sp && atoi(sp)) ? hi_pri : lo_pri));
+  CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->bstream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_trans, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_bcast, cudaEventDisableTiming));
   for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->ev_arrived[i], cudaEventDisableTiming));
-  CK(cudaMalloc(&c->d_counter, FUSED_MAX_SLICES * sizeof(unsigned int)));
-  CK(cudaMemset(c->d_counter, 0, FUSED_MAX_SLICES * sizeof(unsigned int)));
-  CK(cudaMalloc(&c->d_gate_counter, sizeof(unsigned int)));
-  CK(cudaMemset(c->d_gate_counter, 0, sizeof(unsigned int)));
-  {
-    const char *g = getenv("RCV_GATE");
-    const char *fz = getenv("RCV_FUSED");
-    const char *ce = getenv("RCV_CE_GATHER");
-    c->gate = (g ? atoi(g) != 0 : false) && !(fz && atoi(fz)) && !(ce && atoi(ce));
-    const char *pd = getenv("RCV_PDL");
-    c->pdl = pd ? atoi(pd) != 0 : false;  // measured neutral (schedule_ab.txt 8.)
-    const char *bs = getenv("RCV_BCAST_STREAM");
-    // not with the gate: gate + broadcast stream measured slower (N=4
-    // failure-free 1.75 vs 1.66 ms) and hung the multi-GPU tests
-    if ((bs ? atoi(bs) != 0 : true) && !c->gate && !(ce && atoi(ce)))
-    {
-      CK(cudaStreamCreateWithPriority(&c->bstream, cudaStreamNonBlocking, lo_pri));
-      CK(cudaEventCreateWithFlags(&c->ev_bcast, cudaEventDisableTiming));
-    }
-  }
   *out = c;
   return RCV_OK;
 }
@@ -2348,21 +2024,15 @@ int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer
 int rcv_ctx_destroy(rcv_ctx *c) {
   if (!c) return RCV_OK;
   cudaStreamSynchronize(c->side);
+  cudaStreamSynchronize(c->bstream);
   for (auto &r : c->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }
   for (auto e : c->spare_events) cudaEventDestroy(e);
-  cudaEventDestroy(c->ev_main);
-  cudaEventDestroy(c->ev_ready);
+  for (cudaEvent_t e : {c->ev_main, c->ev_ready, c->ev_trans, c->ev_bcast}) cudaEventDestroy(e);
   for (int i = 0; i < 3; ++i) cudaEventDestroy(c->ev_arrived[i]);
-  cudaFree(c->d_counter);
-  cudaFree(c->d_gate_counter);
-  if (c->bstream) {
-    cudaStreamSynchronize(c->bstream);
-    cudaStreamDestroy(c->bstream);
-    cudaEventDestroy(c->ev_bcast);
-  }
+  cudaStreamDestroy(c->bstream);
   cudaStreamDestroy(c->side);
   delete c;
   return RCV_OK;
@@ -2405,43 +2075,17 @@ int rcv_ctx_finish(rcv_ctx *c, uint64_t live_mask, int participate, void *main_s
       c->bstream_dirty = false;
     }
   }
-  int rc = ctx_barrier(c, live_mask, participate != 0, st);
+  // ranks that left after this step's last bucket call: one barrier over the
+  // mask they last took part in
+  int rc = ctx_transition(c, live_mask, st);
+  if (rc) return rc;
+  rc = ctx_barrier(c, live_mask, participate != 0, st);
   if (rc) return rc;
   rc = ctx_flush(c, st, -1);
   if (rc) return rc;
   c->in_step = false;
-  c->fused_in_step = false;
+  c->last_live = 0;  // the closing barrier synchronised every live rank
   return RCV_OK;
-}
-
-static int env_ctas(const char *name, int sms, double dflt_frac) {
-  const char *v = getenv(name);
-  const double f = v ? atof(v) : dflt_frac;
-  if (f <= 0) return 0;                    // 0: uncapped
-  if (f > 2.0) return (int)f;              // an absolute CTA count
-  return std::max(1, (int)(f * sms));      // a fraction of the SMs
-}
-
-// SM shares of the two concurrent streams (profiles/r1/caps_sweep.txt): the
-// NVLink-bound combine saturates the links with about a third of the SMs,
-// and a full-occupancy grid of either kernel would keep the other off the
-// GPU until its last wave drains.  Measured at N=4 on configs[1]: 2.95 ->
-// 2.60 ms/step (failure-free 2.27 -> 1.91, degraded 3.59 -> 3.28); N=2
-// neutral.  RCV_COMB_CTAS / RCV_PRE_CTAS override (0: uncapped).
-constexpr double kCombShare = 0.35, kPreShare = 0.65;
-// A perfect cover (one node per live rank, the failure-free layout) moves
-// the fewest NVLink bytes per HBM byte of pre-reduce, so the pre-reduce sets
-// the cadence and gets the larger share: 0.25 / 0.75 (N=2 failure-free
-// 2.31 -> 2.21 ms; N=4 1.64-1.66 ms at 0.25-0.35, within noise;
-// profiles/r1f/schedule_ab.txt).  RCV_PERFECT_SHARE sets the combine share
-// of perfect covers (0: the fragmented split).
-double comb_share(const rcv_plan_desc *d) {
-  const bool perfect = d->n_comb > 0 && d->n_comb == d->slice_nr;
-  const char *v = getenv("RCV_PERFECT_SHARE");
-  const double f = v ? atof(v) : 0.25;
-  if (perfect && f > 0) return f;
-  const char *fr = getenv("RCV_FRAG_SHARE");  // fragmented covers (experiments)
-  return fr && atof(fr) > 0 ? atof(fr) : kCombShare;
 }
 
 int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
@@ -2450,12 +2094,12 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
   p->set_stride = d->set_stride;
   p->variant = d->variant;
   p->comb_variant = d->comb_variant;
-  if (const char *cv = getenv("RCV_COMB_VARIANT")) p->comb_variant = atoi(cv);  // experiments
   p->live_mask = d->live_mask;
   p->participate = d->participate != 0;
   p->perfect = d->n_comb > 0 && d->n_comb == d->slice_nr;
   p->remote_in = d->remote_in;
   p->remote_out = d->remote_out;
+  const int pre_ctas = env_ctas("RCV_PRE_CTAS", ctx->sms, 1.0 - comb_share(d));
   int off = 0;
   for (int i = 0; i < d->n_pre; ++i) {
     FoldReq r;
@@ -2466,14 +2110,14 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       delete p;
       return rc;
     }
-    r.max_ctas = env_ctas("RCV_PRE_CTAS", ctx->sms, 1.0 - comb_share(d));
+    r.max_ctas = pre_ctas;
     p->pre.push_back(r);
     p->pre_count.push_back(d->pre_counts[i]);
     off += d->pre_counts[i];
   }
   // several full pre-reduce nodes (each 2^level leaves, all present) fuse
   // into one forest launch; plain nodes stay separate requests
-  if (d->n_pre > 1 && d->n_pre <= 8 && getenv("RCV_NO_FOREST") == nullptr) {
+  if (d->n_pre > 1 && d->n_pre <= 8) {
     bool ok = true;
     int total = 0;
     for (int i = 0; i < d->n_pre && ok; ++i) {
@@ -2506,154 +2150,43 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
       r.n_out = d->n_pre;
       r.n_roots = d->n_pre;
       r.acc_dt = d->acc_dtype;
-      r.max_ctas = env_ctas("RCV_PRE_CTAS", ctx->sms, 1.0 - comb_share(d));
+      r.max_ctas = pre_ctas;
       p->has_forest = true;
       p->forest_count = k;
     }
   }
-  if (getenv("RCV_DEBUG")) {
-    fprintf(stderr, "[rcv] rank %d plan: n_pre %d forest %d counts", ctx->me, d->n_pre, (int)p->has_forest);
-    for (int i = 0; i < d->n_pre; ++i) fprintf(stderr, " %d/%u", d->pre_counts[i], d->pre_leaves[i]);
-    fprintf(stderr, " | n_comb %d tree_L %d full_L %d\n", d->n_comb, p->has_comb ? p->comb.tree_L : -9,
-            p->has_comb ? p->comb.full_L : -9);
-  }
-  p->ce_gather = getenv("RCV_CE_GATHER") && atoi(getenv("RCV_CE_GATHER")) && d->participate &&
-                 d->n_comb_out > 1;
-  if (p->ce_gather) {
-    for (int q = 0; q < d->n_comb_out; ++q) p->peer_primary.push_back((const char *)d->comb_out[q]);
-    p->my_primary = (char *)d->comb_out[d->slice_q];
-  }
   if (d->n_comb > 0 && d->participate) {
-    // with the copy-engine gather the combine stores only this rank's slice
-    // into this rank's primary; peers pull it after the next barrier
-    void *const *outs = p->ce_gather ? &d->comb_out[d->slice_q] : d->comb_out;
-    const int n_outs = p->ce_gather ? 1 : d->n_comb_out;
-    int rc = prepare_tree(d->comb_blocks, d->n_comb, d->n_leaves, n_outs, outs,
+    int rc = prepare_tree(d->comb_blocks, d->n_comb, d->n_leaves, d->n_comb_out, d->comb_out,
                           d->acc_dtype, d->divisor, p->comb);
     if (rc) {
       delete p;
       return rc;
     }
     p->comb.max_ctas = env_ctas("RCV_COMB_CTAS", ctx->sms, comb_share(d));
-    {
-      // RCV_WIDE_COMB: 0 off, 1 branchy trees (ProgTree: fragmented covers),
-      // 2 every combine
-      const char *w = getenv("RCV_WIDE_COMB");
-      const int wide = w ? atoi(w) : 1;
-      p->comb.wide32 = wide >= 2 || (wide == 1 && p->comb.full_L < 0);
-      // RCV_PAIR: two vectors per thread for the DIRECT perfect-tree combine
-      const char *pr = getenv("RCV_PAIR");
-      p->comb.pair = pr ? atoi(pr) != 0 : true;
-    }
+    // branchy trees (fragmented covers) evaluate 8-element vectors: half the
+    // control flow per byte (N=2 degraded combine 167 -> 99 us)
+    p->comb.wide32 = p->comb.full_L < 0;
+    // perfect trees over <= 8 nodes: two vectors per thread in flight
+    p->comb.pair = true;
     if (d->guarded) {
       // the combine reads live peers' partials: skip it once one timed out
       p->comb.guard = (const unsigned int *)ctx->bar.status;
       p->comb.guard_mask = (unsigned int)(d->live_mask & ~(1ull << ctx->me));
     }
+    if (d->comb_rank) {
+      for (int i = 0; i < d->n_comb; ++i) {
+        const int rk = d->comb_rank[i];
+        if (rk < 0 || rk >= ctx->n_ranks) {
+          delete p;
+          return set_err(RCV_ERANGE, "rcv_plan_create: cover node %d from rank %d", i, rk);
+        }
+        if (std::find(p->producers.begin(), p->producers.end(), rk) == p->producers.end())
+          p->producers.push_back(rk);
+      }
+    }
     p->has_comb = true;
     p->slice_q = d->slice_q;
     p->slice_nr = d->slice_nr;
-    if (d->slice_w) {
-      uint64_t acc = 0;
-      p->cum_w.push_back(0);
-      for (int q = 0; q < d->slice_nr; ++q) p->cum_w.push_back(acc += d->slice_w[q]);
-      if (acc == 0) {
-        delete p;
-        return set_err(RCV_EINVAL, "rcv_plan_create: owner-slice weights sum to 0");
-      }
-      // the combine's SM share follows this rank's slice (its loads and
-      // stores scale with the slice; the pre-reduce keeps the rest)
-      const char *ss = getenv("RCV_SLICE_SHARE");
-      const double f = (ss && !atoi(ss)) ? 1.0 : (double)d->slice_w[d->slice_q] / (double)acc * d->slice_nr;
-      const double share = std::min(0.7, std::max(0.1, comb_share(d) * f));
-      p->comb.max_ctas = getenv("RCV_COMB_CTAS") ? p->comb.max_ctas : std::max(1, (int)(share * ctx->sms));
-      const int pre_ctas = getenv("RCV_PRE_CTAS") ? -1 : std::max(1, (int)((1.0 - share) * ctx->sms));
-      if (pre_ctas > 0) {
-        for (auto &r : p->pre) r.max_ctas = pre_ctas;
-        p->forest.max_ctas = pre_ctas;
-      }
-    }
-  }
-  // fused kernel: every local node a full perfect subtree (a forest of at
-  // most 8 roots over fp32 leaves), the combine a tree of at most 64 leaves
-  {
-    // the caller decides from the global cover (every live rank must agree:
-    // the ready flags pair launches across ranks); a rank that cannot
-    // honour it fails loudly rather than desynchronising the sequence
-    bool ok = d->participate && p->has_comb && d->slice_nr <= FUSED_MAX_SLICES &&
-              d->n_pre <= 8 && d->acc_dtype == RCV_F32 &&
-              (p->comb.full_L >= 0 || (p->comb.tree_L >= 0 && p->comb.tree_L <= 6));
-    int total = 0;
-    for (int i = 0; i < d->n_pre && ok; ++i) {
-      ok = d->pre_counts[i] == (int)d->pre_leaves[i];
-      total += d->pre_counts[i];
-    }
-    for (int k = 0; k < total && ok; ++k) ok = d->pre_blocks[k].dtype == RCV_F32;
-    ok = ok && total <= RCV_MAX_IN;
-    if (d->fused && !ok) {
-      delete p;
-      return set_err(RCV_EINVAL, "rcv_plan_create: fused plan requested but this rank's cover is not eligible");
-    }
-    if (d->fused) {
-      FusedParams &f = p->ftmpl;
-      memset(&f, 0, sizeof f);
-      int k = 0;
-      for (int i = 0; i < d->n_pre; ++i) {
-        int L = 0;
-        while ((1 << L) < d->pre_counts[i]) ++L;
-        f.root_L[i] = (uint8_t)L;
-        f.root_first[i] = (uint8_t)k;
-        for (int j = 0; j < d->pre_counts[i]; ++j, ++k) f.leaf[k] = (const char *)d->pre_blocks[k].ptr;
-        f.pool_out[i] = (char *)d->pre_out[i];
-      }
-      f.n_leaf = k;
-      f.n_roots = d->n_pre;
-      f.n_node = p->comb.n_in;
-      for (int i = 0; i < f.n_node; ++i) f.node[i] = p->comb.in[i];
-      memcpy(f.node_in, p->comb.node_in, sizeof f.node_in);
-      memcpy(f.present, p->comb.present, sizeof f.present);
-      f.n_out = p->comb.n_out;
-      for (int j = 0; j < f.n_out; ++j) f.out[j] = p->comb.out[j];
-      f.divisor = d->divisor;
-      f.n_slices = d->slice_nr;
-      f.my_slice = d->slice_q;
-      int q = 0;
-      for (int r = 0; r < 64 && q < d->slice_nr; ++r)
-        if ((d->live_mask >> r) & 1ull) f.ready_out[q++] = ctx->bar.peer[r] + 64;
-      f.ready_in = ctx->bar.local + 64;
-      // wait for every live rank, not only those holding cover nodes: a
-      // rank's ready flag also proves it finished reading this pool set
-      // three calls ago, before phase A overwrites it
-      f.producers = (unsigned int)d->live_mask;
-      f.guard_mask = (unsigned int)d->live_mask;
-      f.me = ctx->me;
-      f.counter = ctx->d_counter;
-      f.status = ctx->bar.status;
-      f.timeout_ns = ctx->bar.timeout_ns;
-      const char *fa = getenv("RCV_FUSED_A");
-      const double frac = fa ? atof(fa) : 0.75;
-      const int L = p->comb.full_L >= 0 ? p->comb.full_L : p->comb.tree_L;
-      const bool full = p->comb.full_L >= 0;
-      void (*tab_full[7])(FusedParams) = {
-          fused_bucket_kernel<ProgFull<0>>, fused_bucket_kernel<ProgFull<1>>,
-          fused_bucket_kernel<ProgFull<2>>, fused_bucket_kernel<ProgFull<3>>,
-          fused_bucket_kernel<ProgFull<4>>, fused_bucket_kernel<ProgFull<5>>,
-          fused_bucket_kernel<ProgFull<6>>};
-      void (*tab_tree[7])(FusedParams) = {
-          fused_bucket_kernel<ProgTree<0>>, fused_bucket_kernel<ProgTree<1>>,
-          fused_bucket_kernel<ProgTree<2>>, fused_bucket_kernel<ProgTree<3>>,
-          fused_bucket_kernel<ProgTree<4>>, fused_bucket_kernel<ProgTree<5>>,
-          fused_bucket_kernel<ProgTree<6>>};
-      p->fkern = full ? tab_full[L] : tab_tree[L];
-      // every CTA co-resident (phase-B CTAs spin on flags phase-A CTAs raise)
-      int occ = 1;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->fkern, FUSED_T, 0));
-      const char *fo = getenv("RCV_FUSED_OCC");
-      if (fo) occ = std::min(occ, std::max(1, atoi(fo)));
-      p->fgrid = ctx->sms * std::max(1, occ);
-      f.a_ctas = std::max(1, std::min(p->fgrid - 1, (int)(frac * p->fgrid)));
-      p->fused = true;
-    }
   }
   if (d->n_bcast > 0) {
     FoldReq &r = p->bcast;
@@ -2671,61 +2204,61 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
   return RCV_OK;
 }
 
-}  // extern "C"
-
-namespace {
-
-constexpr int kReadyBase = 128, kDoneBase = 160;  // flag slots (dist.FLAG_SLOTS >= 192)
-
-int launch_gate(rcv_ctx *c, cudaStream_t st, const GateParams &g) {
-  return timed(c, st, 1, 0, 0, 0, [&]() {
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    gate_kernel<<<1, 32, 0, st>>>(g);
-    CK(cudaGetLastError());
-    return RCV_OK;
-  });
+int rcv_plan_destroy(rcv_plan *p) {
+  delete p;
+  return RCV_OK;
 }
 
-// Gated per-bucket schedule of call j (no barrier kernel, no cross-stream
-// events inside the step):
-//   side: broadcasts of calls <= j-3 -> pre-reduce(j) into pool set j%3 ->
-//         gate: release ready = j+1 to every live rank, then acquire every
-//         live rank's done >= j-1 (their combine of call j-2 has read pool
-//         set (j+1)%3 and stored its slices), so the side stream runs at most
-//         two calls ahead of the slowest combine
-//   main: combine(j), whose CTAs acquire ready >= j+1 from every live rank
-//         before the first load and whose last CTA releases done = j+1.
-// A combine that cannot run as one vector launch (ragged slice) or a timed
-// pass takes the explicit form: gate(wait ready) -> combine -> gate(done).
-int plan_bucket_gated(rcv_plan *p, size_t lo, size_t n, cudaStream_t main, cudaStream_t side) {
+// One bucket call j of the step (see include/rcv.h for the schedule).  Three
+// pool sets: call j's pre-reduce overwrites the set last read by the combine
+// of call j-3, which every peer finished before its barrier of call j-2.  So
+// the side stream only waits for that barrier and can run up to two buckets
+// ahead of the combines; the buckets combined at calls <= j-3 are then also
+// complete in this rank's primary.
+int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
+  if (n == 0) return RCV_OK;
   rcv_ctx *c = p->ctx;
+  cudaStream_t main = (cudaStream_t)main_stream;
+  // while timing launch by launch everything runs on the caller's stream, so
+  // each kernel's duration is its own (no cross-stream overlap stretching it)
+  cudaStream_t side = c->timing ? main : c->side;
+  const int es = esize(p->has_comb ? p->comb.acc_dt : RCV_F32);
   if (!c->in_step) {
     // leaves were produced on the caller's stream
     c->in_step = true;
-    c->fused_in_step = false;
     CK(cudaEventRecord(c->ev_main, main));
     CK(cudaStreamWaitEvent(c->side, c->ev_main, 0));
   }
+  int rc = ctx_transition(c, p->live_mask, main);
+  if (rc) return rc;
   const unsigned long long j = c->calls++;
-  const size_t set_off = (j % 3) * p->set_stride;
-  const int es = esize(p->has_comb ? p->comb.acc_dt : RCV_F32);
-  int rc = RCV_OK;
-  // perfect covers broadcast on their own stream behind a done-flag wait
-  // (as in the barrier runtime); fragmented ones on the side stream
-  const bool bstream = c->bstream && !c->timing && p->perfect;
-  if (j >= 3 && !bstream) {
-    if (c->bstream_dirty) {
-      CK(cudaEventRecord(c->ev_bcast, c->bstream));
-      CK(cudaStreamWaitEvent(side, c->ev_bcast, 0));
-      c->bstream_dirty = false;
+  const int set = (int)(j % 3);
+  const size_t set_off = set * p->set_stride;
+  // perfect covers (pre-reduce-bound) broadcast on their own stream right
+  // behind each barrier; fragmented ones (combine-bound) keep them on the
+  // side stream, off the SMs the NVLink-bound combine needs
+  // (profiles/r1f/schedule_ab.txt)
+  const bool bstream = !c->timing && p->perfect;
+  if (j >= 2) {
+    CK(cudaStreamWaitEvent(side, c->ev_arrived[(j - 2) % 3], 0));
+    if (j >= 3 && !bstream) {
+      if (c->bstream_dirty) {
+        // an earlier broadcast of the same bucket may still be on bstream
+        CK(cudaEventRecord(c->ev_bcast, c->bstream));
+        CK(cudaStreamWaitEvent(side, c->ev_bcast, 0));
+        c->bstream_dirty = false;
+      }
+      if ((rc = ctx_flush(c, side, (long long)j - 3))) return rc;
     }
-    if ((rc = ctx_flush(c, side, (long long)j - 3))) return rc;
   }
-  if (!p->participate) return RCV_OK;
+  const bool writes = p->participate && (p->has_forest || !p->pre.empty());
+  if (writes && (rc = stamp_write(c, side, c->stamp_of(c->me, set), 0))) return rc;
   bool forest_done = false;
   if (p->has_forest && n % 64 == 0) {
     FoldReq r = p->forest;
     shift(r, lo, set_off);
+    // the forest evaluator needs 16-byte aligned whole vectors; misaligned
+    // leaves (a caller's odd tensor offsets) take the per-node launches
     if (common_head(r) == 0) {
       const double bytes = (double)(p->forest_count + r.n_out) * n * esize(r.acc_dt);
       if ((rc = timed(c, side, 0, bytes, 0, 0, [&]() { return run_fold(r, n, p->variant, side, c->sms); })))
@@ -2740,238 +2273,31 @@ int plan_bucket_gated(rcv_plan *p, size_t lo, size_t n, cudaStream_t main, cudaS
     if ((rc = timed(c, side, 0, bytes, 0, 0, [&]() { return run_fold(r, n, p->variant, side, c->sms); })))
       return rc;
   }
-  const unsigned int live = (unsigned int)p->live_mask;
-  GateParams ready;
-  memset(&ready, 0, sizeof ready);
-  for (int r = 0; r < c->n_ranks; ++r)
-    if ((live >> r) & 1u) ready.signal[ready.n_signal++] = c->bar.peer[r] + kReadyBase + c->me;
-  ready.signal_value = j + 1;
-  if (j >= 2) {
-    ready.wait_flags = c->bar.local + kDoneBase;
-    ready.wait_value = j - 1;
-    ready.wait_mask = live;
-  }
-  ready.status = c->bar.status;
-  ready.timeout_ns = c->bar.timeout_ns;
-  if ((rc = launch_gate(c, side, ready))) return rc;
-
-  GateParams done;
-  memset(&done, 0, sizeof done);
-  for (int r = 0; r < c->n_ranks; ++r)
-    if ((live >> r) & 1u) done.signal[done.n_signal++] = c->bar.peer[r] + kDoneBase + c->me;
-  done.signal_value = j + 1;
-  done.status = c->bar.status;
-  done.timeout_ns = c->bar.timeout_ns;
+  if (writes && (rc = stamp_write(c, side, c->stamp_of(c->me, set), j + 1))) return rc;
+  CK(cudaEventRecord(c->ev_ready, side));
+  CK(cudaStreamWaitEvent(main, c->ev_ready, 0));
   size_t a = 0, z = 0;
+  std::vector<const unsigned long long *> now;
   if (p->has_comb) {
     const size_t units = (n + 63) / 64;
     a = std::min(n, p->slice_at(units, p->slice_q));
     z = std::min(n, p->slice_at(units, p->slice_q + 1));
+    if (z > a)
+      for (int rk : p->producers) now.push_back(c->stamp_of(rk, set));
   }
-  if (z > a) {
-    FoldReq r = p->comb;
-    shift(r, set_off + a, lo + a);
-    const double sl = (double)(z - a) * es;
-    const double local = (double)(r.n_in - p->remote_in + r.n_out - p->remote_out) * sl;
-    if (!c->timing && single_vec_launch(r, z - a)) {
-      r.gate_flags = c->bar.local + kReadyBase;
-      r.gate_value = j + 1;
-      r.gate_mask = live;
-      r.gate_status = c->bar.status;
-      r.gate_timeout_ns = c->bar.timeout_ns;
-      r.done_counter = c->d_gate_counter;
-      for (int i = 0; i < done.n_signal; ++i) r.done_out[i] = done.signal[i];
-      r.n_done = done.n_signal;
-      r.done_value = j + 1;
-      // waiting CTAs hold their SMs: leave at least half of the GPU to the
-      // pre-reduce they wait for
-      const int cap = std::max(1, c->sms / 2);
-      if (r.max_ctas <= 0 || r.max_ctas > cap) r.max_ctas = cap;
-      rc = timed(c, main, 3, local, p->remote_in * sl, p->remote_out * sl,
-                 [&]() { return run_fold(r, z - a, p->comb_variant, main, c->sms); });
-      if (rc) return rc;
-    } else {
-      GateParams w;
-      memset(&w, 0, sizeof w);
-      w.wait_flags = c->bar.local + kReadyBase;
-      w.wait_value = j + 1;
-      w.wait_mask = live;
-      w.status = c->bar.status;
-      w.timeout_ns = c->bar.timeout_ns;
-      if ((rc = launch_gate(c, main, w))) return rc;
-      rc = timed(c, main, 3, local, p->remote_in * sl, p->remote_out * sl,
-                 [&]() { return run_fold(r, z - a, p->comb_variant, main, c->sms); });
-      if (rc) return rc;
-      if ((rc = launch_gate(c, main, done))) return rc;
-    }
-  } else if ((rc = launch_gate(c, main, done))) {
-    return rc;
-  }
-  if (bstream && j >= 1 && !c->pending.empty()) {
-    // every live rank's combine of call j-1 is done: the buckets combined
-    // at calls <= j-1 are complete in this rank's primary
-    GateParams w;
-    memset(&w, 0, sizeof w);
-    w.wait_flags = c->bar.local + kDoneBase;
-    w.wait_value = j;
-    w.wait_mask = live;
-    w.status = c->bar.status;
-    w.timeout_ns = c->bar.timeout_ns;
-    if ((rc = launch_gate(c, c->bstream, w))) return rc;
-    if ((rc = ctx_flush(c, c->bstream, (long long)j - 1))) return rc;
-    c->bstream_dirty = true;
-  }
-  if (p->has_bcast) {
-    rcv_ctx::Pending e;
-    e.req = p->bcast;
-    e.lo = lo;
-    e.n = n;
-    e.variant = p->variant;
-    e.call = j;
-    c->pending.push_back(e);
-  }
-  return RCV_OK;
-}
-
-}  // namespace
-
-extern "C" {
-
-int rcv_plan_destroy(rcv_plan *p) {
-  delete p;
-  return RCV_OK;
-}
-
-int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
-  if (n == 0) return RCV_OK;
-  rcv_ctx *c = p->ctx;
-  cudaStream_t main = (cudaStream_t)main_stream;
-  // while timing launch by launch everything runs on the caller's stream, so
-  // each kernel's duration is its own (no cross-stream overlap stretching it)
-  cudaStream_t side = c->timing ? main : c->side;
-  const int es = esize(p->has_comb ? p->comb.acc_dt : RCV_F32);
-  if (p->fused) {
-    // one launch: local partials and this rank's slice of the combine,
-    // synchronised per owner slice by ready flags in peer memory
-    c->in_step = true;
-    c->fused_in_step = true;
-    const unsigned long long j = c->calls++;
-    const size_t set_off = (j % 3) * p->set_stride;
-    FusedParams f = p->ftmpl;
-    uintptr_t mis = 0;
-    for (int i = 0; i < f.n_leaf; ++i) mis |= (uintptr_t)(f.leaf[i] += lo * 4);
-    for (int i = 0; i < f.n_roots; ++i) mis |= (uintptr_t)(f.pool_out[i] += set_off * 4);
-    for (int i = 0; i < f.n_node; ++i) mis |= (uintptr_t)(f.node[i] += set_off * 4);
-    for (int i = 0; i < f.n_out; ++i) mis |= (uintptr_t)(f.out[i] += lo * 4);
-    if (mis & 15)
-      return set_err(RCV_EINVAL, "fused bucket: every leaf, pool slot and output must be 16-byte aligned");
-    const size_t nvec = n / 4, units = (n + 63) / 64;
-    for (int q = 0; q < f.n_slices; ++q) f.slice_lo[q] = std::min(n, p->slice_at(units, q)) / 4;
-    f.slice_lo[f.n_slices] = nvec;
-    f.tail = (int)(n % 4);
-    f.seq = ++c->fseq;
-    const double local = (double)(f.n_leaf + f.n_roots) * n * 4;
-    int rc = timed(c, main, 4, local, p->remote_in * (double)n * 4 / f.n_slices,
-                   p->remote_out * (double)n * 4 / f.n_slices, [&]() {
-                     g_launches.fetch_add(1, std::memory_order_relaxed);
-                     p->fkern<<<p->fgrid, FUSED_T, 0, main>>>(f);
-                     CK(cudaGetLastError());
-                     return RCV_OK;
-                   });
-    if (rc) return rc;
-    if (p->has_bcast) {
-      rcv_ctx::Pending e;
-      e.req = p->bcast;
-      e.lo = lo;
-      e.n = n;
-      e.variant = p->variant;
-      e.call = j;
-      e.fused = true;
-      c->pending.push_back(e);
-    }
-    return RCV_OK;
-  }
-  if (c->gate) return plan_bucket_gated(p, lo, n, main, side);
-  if (!c->in_step || c->fused_in_step) {
-    // leaves were produced on the caller's stream (and, after fused
-    // buckets, the pool sets they used are released only in stream order)
-    c->in_step = true;
-    c->fused_in_step = false;
-    CK(cudaEventRecord(c->ev_main, main));
-    CK(cudaStreamWaitEvent(c->side, c->ev_main, 0));
-  }
-  // Three pool sets: call j's pre-reduce overwrites the set last read by the
-  // combine of call j-3, which every peer finished before its barrier of
-  // call j-2.  So the side stream only waits for that barrier and can run
-  // up to two buckets ahead of the combines; the buckets combined at calls
-  // <= j-3 are then also complete in this rank's primary, and their local
-  // broadcasts go here, off the main stream.
-  const unsigned long long j = c->calls++;
-  const size_t set_off = (j % 3) * p->set_stride;
-  // perfect covers (pre-reduce-bound) broadcast on their own stream right
-  // behind each barrier; fragmented ones (combine-bound) keep them on the
-  // side stream, off the SMs the NVLink-bound combine needs
-  // (profiles/r1f/schedule_ab.txt)
-  const bool bstream = c->bstream && !c->timing && p->perfect;
-  if (j >= 2) {
-    CK(cudaStreamWaitEvent(side, c->ev_arrived[(j - 2) % 3], 0));
-    if (j >= 3 && !bstream) {
-      if (c->bstream_dirty) {
-        // an earlier broadcast of the same bucket may still be on bstream
-        CK(cudaEventRecord(c->ev_bcast, c->bstream));
-        CK(cudaStreamWaitEvent(side, c->ev_bcast, 0));
-        c->bstream_dirty = false;
-      }
-      int rc = ctx_flush(c, side, (long long)j - 3);
-      if (rc) return rc;
-    }
-  }
-  bool forest_done = false;
-  if (p->has_forest && n % 64 == 0) {
-    FoldReq r = p->forest;
-    shift(r, lo, set_off);
-    // the forest evaluator needs 16-byte aligned whole vectors; misaligned
-    // leaves (a caller's odd tensor offsets) take the per-node launches
-    if (common_head(r) == 0) {
-      const double bytes = (double)(p->forest_count + r.n_out) * n * esize(r.acc_dt);
-      int rc = timed(c, side, 0, bytes, 0, 0,
-                     [&]() { return run_fold(r, n, p->variant, side, c->sms); });
-      if (rc) return rc;
-      forest_done = true;
-    }
-  }
-  for (size_t i = 0; i < p->pre.size() && !forest_done; ++i) {
-    FoldReq r = p->pre[i];
-    shift(r, lo, set_off);
-    const double bytes = (double)(p->pre_count[i] + 1) * n * esize(r.acc_dt);
-    int rc = timed(c, side, 0, bytes, 0, 0,
-                   [&]() { return run_fold(r, n, p->variant, side, c->sms); });
-    if (rc) return rc;
-  }
-  CK(cudaEventRecord(c->ev_ready, side));
-  CK(cudaStreamWaitEvent(main, c->ev_ready, 0));
-  int rc = ctx_barrier(c, p->live_mask, p->participate, main);
-  if (rc) return rc;
+  if ((rc = ctx_barrier(c, p->live_mask, p->participate, main, &now, j + 1))) return rc;
   CK(cudaEventRecord(c->ev_arrived[j % 3], main));
   if (bstream && j >= 1) {
     // passing barrier j proves every peer finished combine j-1: the buckets
     // combined at calls <= j-1 are complete in this rank's primary
     CK(cudaStreamWaitEvent(c->bstream, c->ev_arrived[j % 3], 0));
-    rc = ctx_flush(c, c->bstream, (long long)j - 1);
-    if (rc) return rc;
+    if ((rc = ctx_flush(c, c->bstream, (long long)j - 1))) return rc;
     c->bstream_dirty = true;
   }
-  if (p->has_comb) {
-    const size_t units = (n + 63) / 64;
-    const size_t a = std::min(n, p->slice_at(units, p->slice_q));
-    const size_t z = std::min(n, p->slice_at(units, p->slice_q + 1));
-    if (z > a) {
+  if (z > a) {
+    {
       FoldReq r = p->comb;
       shift(r, set_off + a, lo + a);
-      // PDL behind the barrier (RCV_PDL=1, opt-in), one vector launch
-      // only: a scalar head would sit between the barrier and the body
-      r.pdl = c->pdl && !c->timing && p->participate &&
-              __builtin_popcountll(p->live_mask) >= 2 && single_vec_launch_any(r, z - a);
       const double sl = (double)(z - a) * es;
       const double local = (double)(r.n_in - p->remote_in + r.n_out - p->remote_out) * sl;
       rc = timed(c, main, 3, local, p->remote_in * sl, p->remote_out * sl,
@@ -2979,24 +2305,7 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
       if (rc) return rc;
     }
   }
-  if (p->ce_gather) {
-    rcv_ctx::Pending e;
-    if (p->has_bcast) e.req = p->bcast;  // else n_out stays 0: gather only
-    e.lo = lo;
-    e.n = n;
-    e.variant = p->variant;
-    e.call = j;
-    e.dst = p->my_primary;
-    e.es = es;
-    const size_t units = (n + 63) / 64;
-    for (int q = 0; q < p->slice_nr; ++q) {
-      if (q == p->slice_q) continue;
-      const size_t a = std::min(n, p->slice_at(units, q));
-      const size_t z = std::min(n, p->slice_at(units, q + 1));
-      e.gather.push_back({p->peer_primary[q], {a, z}});
-    }
-    c->pending.push_back(e);
-  } else if (p->has_bcast) {
+  if (p->has_bcast) {
     rcv_ctx::Pending e;
     e.req = p->bcast;
     e.lo = lo;

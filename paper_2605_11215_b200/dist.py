@@ -49,34 +49,16 @@ from .commit import GradientCommit, aligned_bounds, block_cover
 from .policy import assign_roles, initial_state, policy_advancement
 
 
-# per-rank flag words in peer memory: [0, 64) the step barrier, [64, 128)
-# the fused kernel's per-producer ready sequence, [128, 160) the gated
-# runtime's "partials ready" and [160, 192) its "combine done" sequences
-FLAG_SLOTS = 192
+# per-rank flag words in peer memory: [0, 64) the barrier sequence written by
+# each peer, [64, 67) this rank's pool-set integrity stamps (include/rcv.h)
+FLAG_SLOTS = 128
 
 
-def fused_eligible(cover, slot_of, leaves, ranks, b, acc_code, aligned=True) -> bool:
-    """Whether every live rank can run the fused per-bucket kernel on this
-    cover (RCV_FUSED=1 opts in): fp32, at most 8 perfect local nodes and 64
-    local leaves per rank, at most 64 leaves in the combine tree.  Decided
-    from the global cover so all ranks agree."""
-    if os.environ.get("RCV_FUSED", "0") in ("", "0") or acc_code != _lib.F32:
-        return False
-    if b > 64 or len(ranks) > 32 or not aligned:
-        return False
-    if any(t is not None and (t.dtype != torch.float32 or t.data_ptr() % 16)
-           for _, t in leaves.values()):
-        return False
-    per: Dict[int, List[Tuple[int, int]]] = {}
-    for blo, blev in cover:
-        per.setdefault(slot_of[(blo, blev)][0], []).append((blo, blev))
-    for nodes in per.values():
-        if len(nodes) > 8 or sum(1 << lv for _, lv in nodes) > 64:
-            return False
-        for lo, lv in nodes:
-            if sum(1 for m in leaves if lo <= m < lo + (1 << lv)) != 1 << lv:
-                return False
-    return True
+class CommitIntegrityError(RuntimeError):
+    """A combine read a pool partial whose stamp was not its call's, or that
+    was invalidated while it was being read, or a barrier peer timed out
+    outside real-kill mode: the committed bits of that step are not to be
+    trusted (never silently committed)."""
 
 
 def owner_slice(n: int, q: int, nr: int, align: int = 64):
@@ -87,69 +69,6 @@ def owner_slice(n: int, q: int, nr: int, align: int = 64):
     unequal slices measured slower: profiles/r1/slice_weights.txt)."""
     units = (n + align - 1) // align
     return (min(n, units * q // nr * align), min(n, units * (q + 1) // nr * align))
-
-
-def slice_weights(local_nodes: Sequence[int], n_nodes: int, gain: float = 0.95,
-                  scale: int = 4096) -> Optional[List[int]]:
-    """Owner-slice weights that balance the combine's NVLink directions.
-
-    With owner q holding local_nodes[q] of the n_nodes cover nodes and a
-    share f_q of each bucket (in bucket units): ingress_q = 1 + f_q (n - l_q - 1)
-    (the other nodes' slices it reads, plus the other owners' slices stored
-    into its primary) and egress_q = l_q + f_q (N - 1 - l_q).  Returns integer
-    weights minimising max over q of max(ingress, egress), or None when
-    equal slices are within `gain` of that optimum (a perfect cover always
-    is).  Deterministic: every live rank derives the same weights.
-    Opt-in (RCV_SLICE_BALANCE=1): at N=2 the balanced 3:1 split measured
-    slower than equal slices even with the combine's SM share scaled to the
-    slice — the combine's rate follows its SMs, not this link model."""
-    N = len(local_nodes)
-    if N < 2:
-        return None
-
-    def load(fs):
-        return max(max(1 + f * (n_nodes - l - 1), l + f * (N - 1 - l))
-                   for f, l in zip(fs, local_nodes))
-
-    def feasible(T):
-        los, his = [], []
-        for l in local_nodes:
-            lo, hi = 0.0, 1.0
-            a = n_nodes - l - 1
-            if a > 0:
-                hi = min(hi, (T - 1) / a)
-            elif T < 1:
-                return None
-            b = N - 1 - l
-            if b > 0:
-                hi = min(hi, (T - l) / b)
-            elif b < 0:
-                lo = max(lo, (l - T) / -b)
-            elif l > T:
-                return None
-            if lo > hi:
-                return None
-            los.append(lo)
-            his.append(hi)
-        if sum(los) > 1 or sum(his) < 1:
-            return None
-        rest = 1 - sum(los)
-        room = sum(h - lo for h, lo in zip(his, los)) or 1.0
-        return [lo + (h - lo) * rest / room for h, lo in zip(his, los)]
-
-    t_eq = load([1.0 / N] * N)
-    lo_t, hi_t = 0.0, t_eq
-    best = None
-    for _ in range(50):
-        mid = (lo_t + hi_t) / 2
-        fs = feasible(mid)
-        if fs is None:
-            lo_t = mid
-        else:
-            hi_t, best = mid, fs
-    if best is None or load(best) > gain * t_eq:
-        return None
-    return [max(1, int(round(f * scale))) for f in best]
 
 
 def plan_bucket(owner: Dict[int, int], n_leaves: int, live_ranks: Sequence[int],
@@ -195,35 +114,59 @@ class VmmBuffers:
     POSIX file descriptors, passed to every peer over a Unix socket
     (SCM_RIGHTS) and mapped there.  An importer's mapping holds a reference
     on the physical memory, so a dead peer's buffers never become invalid
-    addresses for the survivors."""
+    addresses for the survivors.
 
-    def __init__(self, rank: int, world: int, group=None):
-        import os
+    The abstract socket is visible to every local process, so the server
+    hands the descriptor only to a peer whose SO_PEERCRED pid is one of the
+    group's and which presents the job's secret (exchanged over the process
+    group); accept, connect and receive are bounded by `timeout_s`."""
+
+    def __init__(self, rank: int, world: int, group=None, timeout_s: float = 60.0):
         import secrets
         self.rank, self.world, self.group = rank, world, group
-        tok = [None] * world
-        dist.all_gather_object(tok, secrets.token_hex(8) if rank == 0 else None, group=group)
-        self.job = tok[0]
+        self.timeout_s = timeout_s
+        got = [None] * world
+        dist.all_gather_object(got, (os.getpid(), secrets.token_hex(16) if rank == 0 else None),
+                               group=group)
+        self.pids = {pid for pid, _ in got}
+        self.secret = got[0][1].encode()
+        self.job = self.secret[:8].decode()
         self.dev = torch.cuda.current_device()
         self._keep = []  # fds and tensors that must outlive the mappings
-        self._os = os
+
+    def _serve(self, srv, fd, errors) -> None:
+        import socket
+        import struct
+        served = 0
+        try:
+            while served < self.world - 1:
+                conn, _ = srv.accept()
+                with conn:
+                    conn.settimeout(self.timeout_s)
+                    cred = conn.getsockopt(socket.SOL_SOCKET, socket.SO_PEERCRED,
+                                           struct.calcsize("3i"))
+                    pid, uid, _ = struct.unpack("3i", cred)
+                    if pid not in self.pids or uid != os.getuid():
+                        continue  # not a rank of this group: refuse
+                    if conn.recv(len(self.secret)) != self.secret:
+                        continue
+                    socket.send_fds(conn, [b"f"], [fd])
+                    served += 1
+        except Exception as exc:  # surfaced by share()
+            errors.append(exc)
 
     def share(self, nbytes: int, dtype: torch.dtype):
         """Allocate nbytes here; returns (local tensor, [ptr of every rank])."""
         import socket
         import threading
         ptr, size, fd = _lib.vmm_alloc(nbytes)
-        addr = "\0rcv-%s-%d-%d" % (self.job, self.rank, len(self._keep))
+        name = "\0rcv-%s-%d-%d"
         srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
-        srv.bind(addr)
+        srv.bind(name % (self.job, self.rank, len(self._keep)))
         srv.listen(self.world)
-
-        def serve():
-            for _ in range(self.world - 1):
-                conn, _ = srv.accept()
-                socket.send_fds(conn, [b"f"], [fd])
-                conn.close()
-        th = threading.Thread(target=serve, daemon=True)
+        srv.settimeout(self.timeout_s)
+        errors: List[Exception] = []
+        th = threading.Thread(target=self._serve, args=(srv, fd, errors), daemon=True)
         th.start()
         meta = [None] * self.world
         dist.all_gather_object(meta, (size, self.dev), group=self.group)
@@ -233,13 +176,19 @@ class VmmBuffers:
                 ptrs.append(ptr)
                 continue
             c = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
-            c.connect("\0rcv-%s-%d-%d" % (self.job, r, len(self._keep)))
+            c.settimeout(self.timeout_s)
+            c.connect(name % (self.job, r, len(self._keep)))
+            c.sendall(self.secret)
             _, fds, _, _ = socket.recv_fds(c, 1, 1)
             c.close()
+            if not fds:
+                raise RuntimeError("rank %d refused its VMM descriptor" % r)
             ptrs.append(_lib.vmm_import(fds[0], meta[r][0], meta[r][1]))
-            self._os.close(fds[0])
-        th.join()
+            os.close(fds[0])
+        th.join(timeout=self.timeout_s)
         srv.close()
+        if errors or th.is_alive():
+            raise RuntimeError("VMM descriptor exchange failed: %r" % (errors or "timeout"))
         es = torch.tensor([], dtype=dtype).element_size()
         local = _lib.tensor_at(ptr, nbytes // es, dtype, torch.device("cuda", self.dev))
         self._keep.append((fd, local))
@@ -278,7 +227,7 @@ class DeadPeerDetector:
         import time
         t0 = time.perf_counter()
         torch.cuda.synchronize(self.engine.device)
-        bits = int(self.engine.status.item()) & ~self.known
+        bits = int(self.engine.status[0].item()) & ~self.known
         if bits:
             self.known |= bits
             dead_ranks = [r for r in range(self.engine.world) if (bits >> r) & 1]
@@ -361,7 +310,13 @@ class DistributedGradientCommit(GradientCommit):
         self.lmax = max(hi - lo for lo, hi in self.bounds)
         self.pool_slots = pool_slots
         self.real_kill = real_kill
-        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        # [0] peers that timed out in a barrier, [1] pool-stamp mismatches
+        self.status = torch.zeros(2, dtype=torch.int32, device=self.device)
+        # each step's status words are copied to pinned memory behind the
+        # step and checked when the next step ends (no host sync on the path)
+        self._status_host = torch.zeros(2, dtype=torch.int32, pin_memory=True)
+        self._status_ev: Optional[torch.cuda.Event] = None
+        self.integrity_errors = 0
         # RCV_TIMEOUT_S overrides every bounded wait (debugging hangs)
         self.timeout_ns = int(float(os.environ.get("RCV_TIMEOUT_S", barrier_timeout_s)) * 1e9)
         if real_kill:
@@ -461,15 +416,42 @@ class DistributedGradientCommit(GradientCommit):
 
     def _end_of_step(self) -> None:
         ranks, mask = self._live_mask()
-        self.rt.finish(mask, self.rank in ranks,
-                       torch.cuda.current_stream(self.device).cuda_stream)
+        stream = torch.cuda.current_stream(self.device)
+        self.rt.finish(mask, self.rank in ranks, stream.cuda_stream)
+        # the previous step's snapshot is complete by now (a step ago);
+        # check it, then snapshot this step's words behind its last kernel
+        if self._status_ev is not None:
+            self._status_ev.synchronize()
+            self._judge(self._status_host.tolist(), "a previous step")
+        self._status_host.copy_(self.status, non_blocking=True)
+        self._status_ev = torch.cuda.Event()
+        self._status_ev.record(stream)
+
+    def _judge(self, words, when: str) -> None:
+        dead, err = int(words[0]) & 0xffffffff, int(words[1]) & 0xffffffff
+        if err:
+            self.integrity_errors += 1
+        if self.real_kill:
+            # a peer's death is detected and recovered by the protocol; a
+            # combine around it may see a stale stamp, and its bucket is
+            # re-reduced over the survivors
+            return
+        if err:
+            raise CommitIntegrityError(
+                "rank %d: a combine in %s read a pool partial with a wrong or invalidated "
+                "stamp (status 0x%x): the committed gradient is not trustworthy"
+                % (self.rank, when, err))
+        if dead:
+            raise CommitIntegrityError(
+                "rank %d: peer ranks 0x%x timed out in a commit barrier in %s (not in "
+                "real-kill mode): their partials may have been read unsynchronised"
+                % (self.rank, dead, when))
 
     def check_peers(self) -> None:
-        """Raise if any barrier so far timed out on a peer (reads the device
-        status word: a host sync, so callers do it off the hot path)."""
-        bad = int(self.status.item())
-        if bad:
-            raise RuntimeError("peer ranks timed out in the commit barrier: mask 0x%x" % bad)
+        """Raise if any barrier so far timed out on a peer or any combine
+        read a partial with a wrong stamp (reads the device status words: a
+        host sync, so callers do it off the hot path)."""
+        self._judge(self.status.tolist(), "this run")
 
     def start_timing(self) -> None:
         self.rt.set_timing(True)
@@ -508,24 +490,18 @@ class DistributedGradientCommit(GradientCommit):
 
         def arr(ctype, xs):
             return (ctype * max(1, len(xs)))(*xs)
-        weights = None
-        # opt-in: measured slower at N=2 (profiles/r1f/schedule_ab.txt 10.)
-        if os.environ.get("RCV_SLICE_BALANCE", "0") not in ("", "0"):
-            per = {rk: 0 for rk in ranks}
-            for rk, _ in slot_of.values():
-                per[rk] += 1
-            weights = slice_weights([per[rk] for rk in ranks], len(cover))
         keep = dict(pre_blocks=arr(Block, pre_blocks), pre_counts=arr(ctypes.c_int, pre_counts),
                     pre_leaves=arr(ctypes.c_uint32, pre_leaves),
                     pre_out=arr(ctypes.c_void_p, pre_out), comb=arr(Block, comb),
                     comb_out=arr(ctypes.c_void_p, [self.grad_ptr[r] for r in prim]),
                     bcast_out=arr(ctypes.c_void_p, [self.grads[r].data_ptr() for r in mine[1:]]),
-                    slice_w=arr(ctypes.c_uint32, weights or []))
+                    comb_rank=arr(ctypes.c_int, [rk for _, (rk, _) in sorted(slot_of.items())]))
         d = _lib.PlanDesc(
             n_pre=len(pre_counts), pre_blocks=keep["pre_blocks"], pre_counts=keep["pre_counts"],
             pre_leaves=keep["pre_leaves"], pre_out=keep["pre_out"],
             set_stride=self.pool_slots * self.lmax,
-            n_comb=len(comb) if part else 0, comb_blocks=keep["comb"], n_leaves=b,
+            n_comb=len(comb) if part else 0, comb_blocks=keep["comb"],
+            comb_rank=keep["comb_rank"], n_leaves=b,
             n_comb_out=len(prim), comb_out=keep["comb_out"],
             slice_q=ranks.index(self.rank) if part else 0, slice_nr=len(ranks),
             n_bcast=max(0, len(mine) - 1),
@@ -535,11 +511,7 @@ class DistributedGradientCommit(GradientCommit):
             live_mask=mask, participate=int(part),
             remote_in=sum(1 for rk, _ in slot_of.values() if rk != self.rank),
             remote_out=sum(1 for r in prim if not self._holds(r)),
-            guarded=int(self.real_kill),
-            fused=int(part and fused_eligible(
-                cover, slot_of, leaves, ranks, b, self._code,
-                aligned=self.lmax % 4 == 0 and self.numel % 4 == 0)),
-            slice_w=keep["slice_w"] if weights else None)
+            guarded=int(self.real_kill))
         self.rt.set_plan(d, keep)
 
     def _reduce_bucket(self, k: int, leaves) -> int:

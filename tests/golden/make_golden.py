@@ -144,6 +144,10 @@ def scripted_scenarios():
                       plans={0: [("during_sync", 1, [0]), ("after_sync", None, [1])]}))
     S.append(scenario("minus_zero_linear_dim5", 5, 1, k=5, kind="linear", dim=5,
                       seed=99, iters=3, plans={1: [("during_sync", 2, [4])]}))
+    # a spare promoted for replica 0 dies later in the same step and a second
+    # spare is promoted for it (round-1 advisor finding, commit.py)
+    S.append(scenario("promoted_spare_dies_same_step", 4, 2, k=4, seed=41, spares=2,
+                      iters=2, plans={0: [("during_sync", 1, [0]), ("during_sync", 2, [4])]}))
     return S
 
 

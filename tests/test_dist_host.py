@@ -10,7 +10,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2605_11215_b200.commit import block_cover
-from paper_2605_11215_b200.dist import DistributedGradientCommit, owner_slice, plan_bucket, slice_weights
+from paper_2605_11215_b200.dist import DistributedGradientCommit, owner_slice, plan_bucket
 
 
 def test_owner_slices_partition():
@@ -137,28 +137,3 @@ def test_dyadic_packing_minimises_cover():
             assert got_n <= cover_size(contiguous, f.rank_of, total)
             if total <= 64:
                 assert got_n <= want
-
-
-
-def test_slice_weights_balance_nvlink_directions():
-    """Owner slices follow the NVLink model of the combine: equal for a
-    perfect cover and for N=4's degraded 2/2/2/3 cover (the 3-node rank's
-    egress is 3 bucket units for any split), 3:1 for N=2's 4 + 2 nodes
-    (busiest direction 2.5 -> 1.75 units)."""
-    assert slice_weights([1, 1], 2) is None
-    assert slice_weights([1, 1, 1, 1], 4) is None
-    assert slice_weights([2, 2, 2, 3], 9) is None
-    w = slice_weights([4, 2], 6)
-    assert w is not None and w[0] == 3 * w[1]
-
-    def load(fs, ls, n):
-        nn = len(ls)
-        return max(max(1 + f * (n - l - 1), l + f * (nn - 1 - l)) for f, l in zip(fs, ls))
-    for ls in ([4, 2], [3, 1], [5, 1, 2], [1, 4, 1, 1]):
-        n = sum(ls)
-        w = slice_weights(ls, n)
-        eq = load([1 / len(ls)] * len(ls), ls, n)
-        if w is None:
-            continue
-        fs = [x / sum(w) for x in w]
-        assert load(fs, ls, n) <= 0.95 * eq + 1e-9
