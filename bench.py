@@ -214,13 +214,14 @@ def reference_step_sample(leaves, fail_bucket=None):
     return _chunked(n, run)
 
 
-def cpu_leg(sample, steps, fail_index):
+def cpu_leg(sample, steps, fail_index, warmup=1):
     """Time the reference algorithm on `sample` elements per step; scale to
     the full gradient.  Returns (tokens/s, seconds per full step, threads)."""
     import numpy as np
     rng = np.random.default_rng(1234)
     leaves = [rng.standard_normal(sample, dtype=np.float32) for _ in range(M)]
-    reference_step_sample(leaves)  # warm caches / page in
+    for _ in range(max(1, warmup)):
+        reference_step_sample(leaves)  # warm caches / page in
     t0 = time.perf_counter()
     nt = 1
     for s in range(steps):
@@ -230,23 +231,40 @@ def cpu_leg(sample, steps, fail_index):
     return M * TOKENS_PER_MB / per_full, per_full, nt
 
 
+def config_dict(args, world):
+    """The workload as both arms report it (identical dicts)."""
+    return {"workload": "gpt2-124m gradient commit, DP=8, M=32, K=%d, replica 3 killed "
+                        "during_sync:%d" % (args.buckets, min(VICTIM_BUCKET, args.buckets - 1)),
+            "numel": args.numel, "replicas": W, "microbatches": M, "buckets": args.buckets,
+            "tokens_per_microbatch": TOKENS_PER_MB,
+            "fail_step": -1 if args.no_fail else args.warmup + args.steps // 2,
+            "placement": "8 replicas on 1 GPU" if world == 1
+            else "%d replicas per rank, NVLink P2P" % (W // world),
+            "l2": "inputs 15.9 GB >> 126 MB L2 (no flush needed)",
+            "parallelism": "dp8-sim" if world == 1 else "dp8 over %d ranks" % world}
+
+
 def run_reference_arm(args):
+    """The reference's CPU data path (oracle port, all host threads) on a
+    bounded sample per step: --warmup untimed steps, then --steps timed
+    ones, the middle one with the failure.  Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    steps = max(1, min(args.steps, 3))
-    tps, per_full, nt = cpu_leg(args.cpu_sample, steps, steps // 2 if not args.no_fail else -1)
+    fail = -1 if args.no_fail else args.steps // 2
+    tps, per_full, nt = cpu_leg(args.cpu_sample, args.steps, fail, warmup=args.warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s",
-        "n_gpus": args.gpus, "steps": steps, "warmup": 1,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per_full * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "gpt2-124m gradient commit, DP=8, M=32, K=20, "
-                               "replica 3 killed during_sync:7", "numel": D_GPT2,
-                   "replicas": W, "microbatches": M, "buckets": K},
+        "config": config_dict(args, world),
         "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": nt, "kind": "port",
-                         "sample": "%d of %d elements per step, %d steps, scaled linearly"
-                                   % (args.cpu_sample, D_GPT2, steps)},
+                         "sample": "%d of %d elements per step (every microbatch gradient, "
+                                   "snapshot, fold and rewind of the reference path on that "
+                                   "slice), %d timed steps, scaled linearly to the full gradient"
+                                   % (args.cpu_sample, D_GPT2, args.steps)},
         "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -259,6 +277,62 @@ def run_reference_arm(args):
 def _lib_launches():
     from paper_2605_11215_b200 import _lib
     return _lib.launch_count()
+
+
+def torch_reference_tree(leaves, lo, hi, b):
+    """The canonical dyadic tree of leaves[lo:hi] (all b present, b a power
+    of two) divided by b, evaluated with plain torch fp32 ops: IEEE
+    round-to-nearest adds level by level and a true division; independent of
+    librcv (the bench's parity check)."""
+    vals = [t[lo:hi] for t in leaves]
+    while len(vals) > 1:
+        vals = [vals[i] + vals[i + 1] for i in range(0, len(vals), 2)]
+    return vals[0] / float(b)
+
+
+def parity_check(eng, leaves, numel, chunk=1 << 24):
+    """Bitwise comparison of every live replica this rank holds against the
+    torch reference tree; returns the number of mismatching elements."""
+    import torch
+    mine = [r for r in eng.comm.members if r in eng.grads]
+    bad = 0
+    for lo in range(0, numel, chunk):
+        hi = min(numel, lo + chunk)
+        want = torch_reference_tree(leaves, lo, hi, M)
+        for r in mine:
+            bad += int((eng.grads[r][lo:hi].view(torch.int32) != want.view(torch.int32)).sum())
+    return bad
+
+
+def recovery_breakdown(eng):
+    """Device-time split of the failure step from the engine's recovery
+    marks: FAILURE -> first recomputed microbatch (the protocol's repair
+    and quota decisions on the host, device still draining the first pass),
+    recompute (regenerating the dead replica's uncommitted microbatch
+    gradients on the survivors), re-reduce (every bucket committed after the
+    recompute, the step's closing barrier included).  The parts sum to the
+    total, FAILURE -> commit."""
+    ev = eng.recovery_events or []
+    names = [n for n, _, _ in ev]
+    if "fail" not in names or "commit" not in names:
+        return None
+    fail = ev[names.index("fail")]
+    commit = ev[len(names) - 1 - names[::-1].index("commit")]
+    regen = [(a, z) for (na, a, _), (nz, z, _) in zip(ev, ev[1:]) if na == "regen_a" and nz == "regen_b"]
+    total = fail[1].elapsed_time(commit[1])
+    if regen:
+        first, last = regen[0][0], regen[-1][1]
+        reform = fail[1].elapsed_time(first)
+        recompute = sum(a.elapsed_time(z) for a, z in regen)
+        gaps = first.elapsed_time(last) - recompute
+        rereduce = last.elapsed_time(commit[1]) + gaps
+    else:
+        reform, recompute, rereduce = 0.0, 0.0, total
+    return {"total_ms": total, "detect_ms": 0.0, "reform_ms": reform,
+            "recompute_ms": recompute, "rereduce_ms": rereduce,
+            "recomputed_microbatches": len(regen),
+            "reform_host_ms": None, "detect_note": "simulated kill: the injector reports the "
+            "death at the collective (real detection: tools/realkill_bench.py)"}
 
 
 def run_ours(args):
@@ -275,12 +349,16 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     numel = args.numel
 
-    # synthetic per-microbatch gradients (the backward outputs), in HBM
-    # the same generator sequence on every rank: microbatch m's gradient has
-    # the same bits wherever it is (re)computed (canonical addressing)
-    gen = torch.Generator(device=dev).manual_seed(1234)
-    leaves = [torch.randn(numel, generator=gen, device=dev, dtype=torch.float32)
-              for _ in range(M)]
+    # synthetic per-microbatch gradients (the backward outputs), resident in
+    # HBM.  Microbatch m's gradient is a function of m alone (its own seeded
+    # generator), so a survivor that recomputes it gets the same bits.
+    def make_leaf(m, out=None):
+        gen = torch.Generator(device=dev).manual_seed(1234 + m)
+        if out is None:
+            return torch.randn(numel, generator=gen, device=dev, dtype=torch.float32)
+        return torch.randn(numel, generator=gen, device=dev, dtype=torch.float32, out=out)
+
+    leaves = [make_leaf(m) for m in range(M)]
     total_steps = args.warmup + args.steps
     fail_step = -1 if args.no_fail else args.warmup + args.steps // 2
     if args.trace and args.trace_degraded:
@@ -294,14 +372,28 @@ def run_ours(args):
                              variant=args.variant)
     kill = StepKill(fail_step, min(VICTIM_BUCKET, args.buckets - 1))
 
+    # the failure step charges real work for the microbatches the dead
+    # replica had not committed: a survivor that takes one over regenerates
+    # its gradient on the device (standing in for that microbatch's
+    # backward), bracketed by recovery marks
+    victim_range = set(range(VICTIM * G, (VICTIM + 1) * G))
+    regen_bufs = {}
+    regen_done = {}
+
     def leaf(m, rid):
+        if kill.step == kill.at_step and m in victim_range and rid != VICTIM:
+            if regen_done.get(m) != kill.step:
+                buf = regen_bufs.setdefault(m, torch.empty_like(leaves[m]))
+                eng.mark("regen_a")
+                make_leaf(m, out=buf)
+                eng.mark("regen_b")
+                regen_done[m] = kill.step
+            return regen_bufs[m]
         return leaves[m]
 
-    # reference layout of the group for the e2e leg is identical; warm up
     stream = torch.cuda.current_stream(dev)
     step_ev = []
     outcomes = []
-    launches = 0
     for s in range(args.warmup):
         kill.step = s
         eng.step(s, leaf, kill)
@@ -331,6 +423,7 @@ def run_ours(args):
     recs = eng.drain_timing()
     if world > 1:
         torch.distributed.barrier()
+    eng.recovery_events = []
     n_launch0 = _lib_launches()
     with Clocks(local) as clk:
         start = torch.cuda.Event(enable_timing=True)
@@ -341,9 +434,7 @@ def run_ours(args):
             kill.step = s
             a = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            out = eng.step(s, leaf, kill)
-            outcomes.append(out)
-            launches += out.launches
+            outcomes.append(eng.step(s, leaf, kill))
             step_ev.append(a)
         end.record(stream)
         host_ms = (time.perf_counter() - t_host) * 1e3 / args.steps
@@ -359,6 +450,21 @@ def run_ours(args):
     committed = sum(o.contrib_total for o in outcomes)
     tokens = committed * TOKENS_PER_MB
     value = tokens / (elapsed_ms / 1e3)
+    fail_idx = [i for i, o in enumerate(outcomes) if o.events]
+    recovery = recovery_breakdown(eng) if fail_idx else None
+    if recovery is not None:
+        recovery["reform_host_ms"] = outcomes[fail_idx[0]].reform_host_s * 1e3
+    eng.recovery_events = None
+
+    # the bench proves its own number: after the timed region every live
+    # replica's committed gradient (the last step's, degraded layout when a
+    # replica died) must equal the canonical tree evaluated independently
+    # with plain torch ops, bit for bit
+    mism = parity_check(eng, leaves, numel)
+    if world > 1:
+        t = torch.tensor([mism], device=dev, dtype=torch.int64)
+        torch.distributed.all_reduce(t)
+        mism = int(t.item())
 
     # the same per-kernel pass over 2 steps of the degraded layout (after the
     # timed region, so the headline is unperturbed)
@@ -376,17 +482,12 @@ def run_ours(args):
     per_kind_deg = summarise_kernels(recs_deg)[1]
     peak, peak_kind = peaks()
     dom = max(kinds, key=lambda kk: kinds[kk]["ms"]) if kinds else None
-    fail_idx = [i for i, o in enumerate(outcomes) if o.events]
-    # recovery: the failure step against the failure-free steps before it
-    # (the steps after it run the degraded layout, reported separately)
+    # the failure step against the failure-free steps before it (the steps
+    # after it run the degraded layout, reported separately)
     pre = step_ms[:fail_idx[0]] if fail_idx else step_ms
     post = step_ms[fail_idx[-1] + 1:] if fail_idx else []
-    recovery_ms = (step_ms[fail_idx[0]] - statistics.median(pre)) if fail_idx and pre else None
-
-    # correctness spot check inside the bench: every live replica holds the
-    # same bytes (one kernel wrote them all)
-    mine = [r for r in eng.comm.members if r in eng.grads]
-    agree = all(torch.equal(eng.grads[r], eng.grads[mine[0]]) for r in mine[1:])
+    if recovery is not None and pre:
+        recovery["failure_step_extra_ms"] = step_ms[fail_idx[0]] - statistics.median(pre)
 
     # e2e through the public API with host buffers: pinned host gradients
     # copied in every step, committed gradient copied out every step
@@ -402,26 +503,24 @@ def run_ours(args):
         "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": "gpt2-124m gradient commit, DP=8, M=32, K=%d, "
-                               "replica 3 killed during_sync:%d" % (args.buckets, kill.bucket),
-                   "numel": numel, "replicas": W, "microbatches": M, "buckets": args.buckets,
-                   "tokens_per_microbatch": TOKENS_PER_MB,
-                   "fail_step": fail_step, "placement": "8 replicas on 1 GPU" if world == 1
-                   else "%d replicas per rank, NVLink P2P" % (W // world), "l2": "inputs 15.9 GB >> 126 MB L2",
-                   "parallelism": "dp8-sim"},
+        "config": config_dict(args, world),
+        "parity": "bitwise" if mism == 0 else "fail",
+        "parity_detail": {"mismatched_elements": mism, "checked": "every live replica's "
+                          "committed gradient after the timed region vs a torch fp32 "
+                          "canonical tree / B over all %d microbatch gradients" % M},
         "roofline": roofline(dom, per_kind, peak, peak_kind, world),
         "kernels": per_kind,
         "kernels_degraded": per_kind_deg or None,
         # masked-allreduce algorithmic bandwidth: gradient bytes committed
         # (reduced over the live replicas and scaled) per second of step time
         "allreduce_algbw_gbs": numel * 4 / (elapsed_ms / args.steps / 1e3) / 1e9,
-        "recovery_ms": recovery_ms,
+        "recovery_ms": recovery["total_ms"] if recovery else None,
+        "recovery": recovery,
         "step_ms": {"median": statistics.median(step_ms), "max": max(step_ms),
                     "failure_step": step_ms[fail_idx[0]] if fail_idx else None,
                     "failure_free_median": statistics.median(pre) if pre else None,
                     "degraded_median": statistics.median(post) if post else None,
                     "all": [round(x, 3) for x in step_ms]},
-        "replica_agreement": agree,
         "host_enqueue_ms_per_step": host_ms,
         "gpu_launches": n_launch,
         "kernel_pass": "per-kernel rows from 3 failure-free steps timed launch by launch (CUDA events on each launch's stream) before the headline region",
@@ -437,12 +536,26 @@ def run_ours(args):
         print(json.dumps(line))
     if world > 1:
         torch.distributed.destroy_process_group()
+    if mism:
+        sys.exit(3)
 
 
 NVLINK_PEAK = 770.0  # GB/s per direction, measured peer copy (B200_PROFILING.md)
-# dram read+write bytes per launch of the dominant kernel, ncu --set full
-# (profiles/r1/ncu_full_fold_direct_ProgFull5.txt: 796.4 MB + 147.9 MB)
-TRAFFIC = {"fused": 944.3e6}
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def traffic_of(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the committed ncu --set full capture of this build
+    (profiles/ncu_traffic.json, written by tools/ncu_summarize.py traffic),
+    or None when no capture of that kernel is committed."""
+    try:
+        with open(TRAFFIC_FILE) as f:
+            d = json.load(f)
+    except (OSError, ValueError):
+        return None
+    row = d.get("kernels", {}).get(kernel)
+    return None if row is None else row.get("dram_bytes")
 
 
 def summarise_kernels(recs):
@@ -490,7 +603,7 @@ def roofline(dom, per_kind, peak, peak_kind, world=1):
                 "hbm_gbs": k["hbm_gbs"]}
     return {"bound": "hbm", "achieved": k["hbm_gbs"], "peak": peak, "unit": "GB/s",
             "frac": k["hbm_gbs"] / peak if k["hbm_gbs"] else None,
-            "traffic": TRAFFIC.get(dom), "peak_kind": peak_kind,
+            "traffic": traffic_of("fold_direct_kernel<float, ProgFull<5>>"), "peak_kind": peak_kind,
             "kernel": "fold_direct_kernel<float, ProgFull<L>> (rcv_tree_commit AUTO, %s)" % dom,
             "mean_launch_us": k["mean_launch_us"], "launches_timed": k["launches"]}
 

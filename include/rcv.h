@@ -115,6 +115,26 @@ int rcv_masked_allreduce_multidev(void *const *views, int n,
 int rcv_accumulate(void *acc, const void *grad, int acc_dtype, int grad_dtype,
                    size_t numel, int first, void *stream);
 
+/* K-ACC: one push of the canonical dyadic accumulator (SURVEY §7.3 R1,
+ * §8(b)), the B200 replacement of the per-microbatch `flat += grad`
+ * (trainer.py:202-229).  A replica's microbatch gradients enter a
+ * binary-counter stack of canonical-tree nodes; pushing microbatch m merges
+ * it with the c stack entries it completes, in one pass:
+ *     out = stack[0] + (stack[1] + (... + (stack[c-1] + grad)))
+ * where stack[c-1] is the top (the left sibling of m's leaf) and stack[0]
+ * the deepest merged node; `out` may alias stack[0] (elementwise, in place)
+ * or be a fresh slot when c == 0.  The gradient arrives as it leaves
+ * backward, one segment per parameter tensor (seg_ptr[i] holds seg_len[i]
+ * elements of flat positions [seg_off[i], seg_off[i] + seg_len[i])), so
+ * nothing is copied into a flat buffer first.  Segments must be ascending,
+ * contiguous from 0, each a multiple of 4 elements and 16-byte aligned
+ * (8-byte for bf16); n_seg <= 256, c <= 8.  Every add is round-to-nearest
+ * fp32, so a node's value is bitwise the canonical subtree's. */
+int rcv_kacc_push(const void *const *seg_ptr, const uint64_t *seg_off,
+                  const uint64_t *seg_len, int n_seg, int grad_dtype,
+                  const float *const *stack, int c, float *out, size_t numel,
+                  void *stream);
+
 /* Canonical-order commit (the B200 design): `blocks` are
  * partial sums of aligned dyadic microbatch-index blocks [lo, lo+2^level)
  * over a canonical binary tree of next_pow2(n_leaves) leaves, empty leaves
@@ -262,6 +282,11 @@ int rcv_ctx_destroy(rcv_ctx *ctx);
 int rcv_ctx_finish(rcv_ctx *ctx, uint64_t live_mask, int participate,
                    void *main_stream);
 int rcv_ctx_set_timing(rcv_ctx *ctx, int on);
+/* Real-kill mode: the node's liveness dead word (rcv_liveness_dead_word,
+ * device pointer) that barrier kernels consult while they wait: a peer
+ * declared dead is neither waited for nor signalled (status word 0 gets its
+ * bit, guarded combines skip). NULL detaches. */
+int rcv_ctx_set_liveness(rcv_ctx *ctx, const uint32_t *device_dead_word);
 /* Drain recorded launch timings (call after synchronising): up to `max`
  * entries of kind (0 pre-reduce, 1 barrier, 2 broadcast, 3 combine),
  * milliseconds, algorithmic HBM bytes, NVLink in / out bytes. */
@@ -298,6 +323,30 @@ typedef struct {
 int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *desc, rcv_plan **out);
 int rcv_plan_destroy(rcv_plan *plan);
 int rcv_plan_bucket(rcv_plan *plan, size_t lo, size_t n, void *main_stream);
+
+/* ---- node-local liveness (real-kill mode; live.cpp) ----------------------
+ * Replaces a barrier-timeout detection with a heartbeat: every rank's native
+ * thread stamps its slot of the POSIX shared-memory segment `name` every
+ * period_ns (CLOCK_MONOTONIC); a peer whose stamp is older than deadline_ns,
+ * or whose process is gone, gets its bit OR-ed into the segment's dead word.
+ * The segment is registered as mapped host memory, so every GPU's barrier
+ * kernel reads the word while it waits (rcv_ctx_set_liveness).  Agreement:
+ * poll point `seq` (1, 2, ... in the replicated control flow) is decided by
+ * the first rank reaching it, which compare-and-swaps the current dead word
+ * into the segment's decision ring; every rank gets the same mask back for
+ * the same seq (the survivors' common view of comm.py:129-172's failed set). */
+typedef struct rcv_liveness rcv_liveness;
+int rcv_liveness_create(const char *name, int rank, int world, uint64_t period_ns,
+                        uint64_t deadline_ns, rcv_liveness **out);
+int rcv_liveness_dead_word(rcv_liveness *lv, const uint32_t **device_ptr, uint32_t *now);
+int rcv_liveness_decide(rcv_liveness *lv, uint64_t seq, uint32_t *mask_out,
+                        uint64_t *decided_ns);
+/* Per-rank timestamps (CLOCK_MONOTONIC ns): last heartbeat, first declared
+ * dead (0: alive), self-reported kill (benchmarks), and the clock now. */
+int rcv_liveness_stats(rcv_liveness *lv, int rank, uint64_t *beat_ns, uint64_t *dead_ns,
+                       uint64_t *kill_ns, uint64_t *now);
+int rcv_liveness_note_kill(rcv_liveness *lv);
+int rcv_liveness_destroy(rcv_liveness *lv, int unlink_name);
 
 #ifdef __cplusplus
 }

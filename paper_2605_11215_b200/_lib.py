@@ -32,7 +32,9 @@ EXPORTS = (
     "rcv_ipc_export", "rcv_ipc_import", "rcv_barrier", "rcv_tree_commit_at",
     "rcv_ctx_create", "rcv_ctx_destroy", "rcv_ctx_finish", "rcv_ctx_set_timing",
     "rcv_ctx_timing", "rcv_plan_create", "rcv_plan_destroy", "rcv_plan_bucket",
-    "rcv_vmm_alloc", "rcv_vmm_import",
+    "rcv_vmm_alloc", "rcv_vmm_import", "rcv_kacc_push", "rcv_ctx_set_liveness",
+    "rcv_liveness_create", "rcv_liveness_dead_word", "rcv_liveness_decide",
+    "rcv_liveness_stats", "rcv_liveness_note_kill", "rcv_liveness_destroy",
 )
 
 
@@ -127,6 +129,16 @@ def load() -> ctypes.CDLL:
         "rcv_plan_bucket": (i32, [vp, sz, sz, vp]),
         "rcv_vmm_alloc": (i32, [sz, ctypes.POINTER(vp), ctypes.POINTER(sz), ctypes.POINTER(i32)]),
         "rcv_vmm_import": (i32, [i32, sz, i32, ctypes.POINTER(vp)]),
+        "rcv_kacc_push": (i32, [pvp, ctypes.POINTER(u64), ctypes.POINTER(u64), i32, i32,
+                                pvp, i32, vp, sz, vp]),
+        "rcv_ctx_set_liveness": (i32, [vp, vp]),
+        "rcv_liveness_create": (i32, [ctypes.c_char_p, i32, i32, u64, u64, ctypes.POINTER(vp)]),
+        "rcv_liveness_dead_word": (i32, [vp, ctypes.POINTER(vp), ctypes.POINTER(u32)]),
+        "rcv_liveness_decide": (i32, [vp, u64, ctypes.POINTER(u32), ctypes.POINTER(u64)]),
+        "rcv_liveness_stats": (i32, [vp, i32, ctypes.POINTER(u64), ctypes.POINTER(u64),
+                                     ctypes.POINTER(u64), ctypes.POINTER(u64)]),
+        "rcv_liveness_note_kill": (i32, [vp]),
+        "rcv_liveness_destroy": (i32, [vp, i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -250,6 +262,39 @@ def accumulate(acc: torch.Tensor, grad: torch.Tensor, first: bool = False) -> No
     _check(load().rcv_accumulate(acc.data_ptr(), grad.data_ptr(),
                                  dtype_code(acc), dtype_code(grad),
                                  acc.numel(), int(first), stream_of(acc)))
+
+
+KACC_MAX_SEGS, KACC_MAX_DEPTH = 256, 8
+
+
+def kacc_push(grads: Sequence[torch.Tensor], stack: Sequence[torch.Tensor],
+              out: torch.Tensor) -> None:
+    """rcv_kacc_push: out = stack[0] + (... + (stack[-1] + flat(grads))),
+    where flat(grads) is the concatenation of the per-parameter gradient
+    tensors in order (read in place, no flattening copy).  out may be
+    stack[0] (in-place merge) or a fresh buffer (empty stack)."""
+    require_cuda(out, "K-ACC output")
+    n = len(grads)
+    if n == 0 or n > KACC_MAX_SEGS:
+        raise ValueError("K-ACC takes 1..%d gradient segments, got %d" % (KACC_MAX_SEGS, n))
+    if len(stack) > KACC_MAX_DEPTH:
+        raise ValueError("K-ACC carry chain longer than %d" % KACC_MAX_DEPTH)
+    dt = dtype_code(grads[0])
+    ptrs = (ctypes.c_void_p * n)()
+    offs = (ctypes.c_uint64 * n)()
+    lens = (ctypes.c_uint64 * n)()
+    pos = 0
+    for i, g in enumerate(grads):
+        if not g.is_cuda or not g.is_contiguous() or dtype_code(g) != dt:
+            raise ValueError("K-ACC gradient segment %d must be a contiguous CUDA tensor of one "
+                             "dtype" % i)
+        ptrs[i], offs[i], lens[i] = g.data_ptr(), pos, g.numel()
+        pos += g.numel()
+    for s in stack:
+        require_cuda(s, "K-ACC stack entry")
+    st = _ptrs(stack)
+    _check(load().rcv_kacc_push(ptrs, offs, lens, n, dt, st, len(stack), out.data_ptr(),
+                                out.numel(), stream_of(out)))
 
 
 def tree_program(blocks: Sequence[tuple], n_leaves: int):
@@ -441,6 +486,9 @@ class BucketRuntime:
     def set_timing(self, on: bool) -> None:
         _check(load().rcv_ctx_set_timing(self.ctx, int(on)))
 
+    def set_liveness(self, lv: Optional["Liveness"]) -> None:
+        _check(load().rcv_ctx_set_liveness(self.ctx, lv.device_word if lv else None))
+
     def timings(self, max_n: int = 1 << 16):
         kind = (ctypes.c_int * max_n)()
         ms = (ctypes.c_float * max_n)()
@@ -496,3 +544,43 @@ def tensor_at(ptr: int, numel: int, dtype: torch.dtype, device) -> torch.Tensor:
                torch.int32: "<i4"}[dtype]
     with torch.cuda.device(device):
         return torch.as_tensor(_CudaArray(ptr, numel, typestr), device=device)
+
+
+class Liveness:
+    """rcv_liveness: node-local heartbeat and failed-set agreement of one
+    rank (include/rcv.h).  Every rank of the group must create it with the
+    same `name` before any of them relies on it (a barrier after create)."""
+
+    def __init__(self, name: str, rank: int, world: int, period_s: float = 1e-3,
+                 deadline_s: float = 10e-3):
+        h = ctypes.c_void_p(0)
+        _check(load().rcv_liveness_create(name.encode(), rank, world, int(period_s * 1e9),
+                                          int(deadline_s * 1e9), ctypes.byref(h)))
+        self.h, self.rank, self.world, self.name = h, rank, world, name
+        dp, now = ctypes.c_void_p(0), ctypes.c_uint32(0)
+        _check(load().rcv_liveness_dead_word(self.h, ctypes.byref(dp), ctypes.byref(now)))
+        self.device_word = dp.value
+
+    def dead(self) -> int:
+        now = ctypes.c_uint32(0)
+        _check(load().rcv_liveness_dead_word(self.h, None, ctypes.byref(now)))
+        return now.value
+
+    def decide(self, seq: int):
+        """(agreed dead mask, CLOCK_MONOTONIC ns it was decided) of poll seq."""
+        m, t = ctypes.c_uint32(0), ctypes.c_uint64(0)
+        _check(load().rcv_liveness_decide(self.h, seq, ctypes.byref(m), ctypes.byref(t)))
+        return m.value, t.value
+
+    def stats(self, rank: int) -> dict:
+        v = [ctypes.c_uint64(0) for _ in range(4)]
+        _check(load().rcv_liveness_stats(self.h, rank, *[ctypes.byref(x) for x in v]))
+        return dict(beat_ns=v[0].value, dead_ns=v[1].value, kill_ns=v[2].value, now_ns=v[3].value)
+
+    def note_kill(self) -> None:
+        _check(load().rcv_liveness_note_kill(self.h))
+
+    def close(self, unlink: bool = False) -> None:
+        if self.h:
+            load().rcv_liveness_destroy(self.h, int(unlink))
+            self.h = None

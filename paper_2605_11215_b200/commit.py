@@ -99,6 +99,22 @@ def block_cover(owner: Dict[int, object], n_leaves: int,
     return out
 
 
+def input_nodes(leaves) -> List[Tuple[int, int, torch.Tensor]]:
+    """The commit's inputs, ascending: (lo, level, tensor) per distinct
+    canonical-tree node of a leaf set {m: (rid, value)} whose values are
+    microbatch gradients (the node (m, 0)) or K-ACC nodes (kacc.KNode: a
+    complete subtree, shared by every index it covers)."""
+    seen, out = set(), []
+    for m in sorted(leaves):
+        v = leaves[m][1]
+        if isinstance(v, torch.Tensor):
+            out.append((m, 0, v))
+        elif id(v) not in seen:
+            seen.add(id(v))
+            out.append((v.lo, v.level, v.tensor))
+    return out
+
+
 @dataclass
 class CommitOutcome:
     """Mirror of IterationOutcome (trainer.py:232-252) for the engine."""
@@ -121,6 +137,7 @@ class CommitOutcome:
     boundary_crossed: bool = False
     launches: int = 0
     failure_wall_s: Optional[float] = None  # host wall from first FAILURE to commit
+    reform_host_s: float = 0.0  # host time in the failure handling (repair, policy, roles)
 
 
 class GradientCommit:
@@ -155,6 +172,8 @@ class GradientCommit:
         self._plan_cache = None
         # optional launch timing: list of (start_event, end_event, algo_bytes, kind)
         self.timing: Optional[list] = None
+        # optional recovery trace: [(name, CUDA event, host time)] marks
+        self.recovery_events: Optional[list] = None
         _lib.enable_peer_access(sorted({d.index for d in self.placement.values()}))
 
     # ---- data plane ----
@@ -185,6 +204,21 @@ class GradientCommit:
     def _end_of_step(self) -> None:
         """Hook run after the last bucket of a step is committed."""
 
+    def _stream_device(self) -> torch.device:
+        """Device whose current stream carries the commit's tail."""
+        return self.placement[self.comm.members[0]] if self.comm.members else \
+            next(iter(self.placement.values()))
+
+    def mark(self, name: str) -> None:
+        """Record a named CUDA event on the commit stream (recovery trace:
+        'fail' at the first FAILURE, 'commit' after the step's last kernel;
+        callers add their own, e.g. around recomputed microbatches)."""
+        if self.recovery_events is None:
+            return
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(torch.cuda.current_stream(self._stream_device()))
+        self.recovery_events.append((name, ev, time.perf_counter()))
+
     def _scratch_buf(self, dev: torch.device, i: int) -> torch.Tensor:
         """Full-length partial buffer i on dev (multi-device covers only):
         bucket k's partial lives at the bucket's own offset, so partials and
@@ -207,27 +241,26 @@ class GradientCommit:
         outs = [self.grads[r] for r in members]
         owner = {m: self.placement[rid] for m, (rid, _) in leaves.items()}
         cover = block_cover(owner, b)
+        nodes = input_nodes(leaves)
         pre = []
         if len(cover) == 1:
             # every present leaf on one device: one fused launch per bucket
-            ins = [(leaves[m][1].data_ptr(), m, 0, _lib.dtype_code(leaves[m][1]))
-                   for m in sorted(leaves)]
+            ins = [(t.data_ptr(), lo, lev, _lib.dtype_code(t)) for lo, lev, t in nodes]
             top_dev = owner[min(leaves)]
         else:
             ins, used = [], {}
             for blo, blev in cover:
-                span = [m for m in sorted(leaves) if blo <= m < blo + (1 << blev)]
-                dev = owner[span[0]]
-                if len(span) == 1:
-                    t = leaves[span[0]][1]
-                    ins.append((t.data_ptr(), blo, blev, _lib.dtype_code(t)))
+                sub = [n for n in nodes if blo <= n[0] < blo + (1 << blev)]
+                dev = owner[sub[0][0]]
+                if len(sub) == 1:
+                    lo, lev, t = sub[0]
+                    ins.append((t.data_ptr(), lo, lev, _lib.dtype_code(t)))
                     continue
                 buf = self._scratch_buf(dev, used.get(dev, 0))
                 used[dev] = used.get(dev, 0) + 1
-                sub = [(leaves[m][1].data_ptr(), m - blo, 0, _lib.dtype_code(leaves[m][1]))
-                       for m in span]
-                pre.append((dev, _lib.TreePlan(sub, 1 << blev, [buf.data_ptr()], acc, 0.0,
-                                               self.variant)))
+                pre.append((dev, _lib.TreePlan(
+                    [(t.data_ptr(), lo - blo, lev, _lib.dtype_code(t)) for lo, lev, t in sub],
+                    1 << blev, [buf.data_ptr()], acc, 0.0, self.variant)))
                 ins.append((buf.data_ptr(), blo, blev, acc))
             top_dev = self.placement[members[0]]
         top = _lib.TreePlan(ins, b, [o.data_ptr() for o in outs], acc, float(b), self.variant)
@@ -360,6 +393,7 @@ class GradientCommit:
         after_fired = False
         touched = set()
         t_fail: Optional[float] = None
+        reform_s = 0.0
 
         def live():
             return [r for r in comm.members if self.alive[r]]
@@ -401,6 +435,11 @@ class GradientCommit:
                     continue      # virtual zeroing: spare work never enters
                 for i in admitted.get(rid, ()):
                     lv[i] = (rid, leaf(i, rid) if self._holds(rid) else None)
+            # K-ACC leaves resolve to their stack node once every admitted
+            # microbatch of this leaf set has been pushed
+            for i, (rid, v) in lv.items():
+                if hasattr(v, "resolve"):
+                    lv[i] = (rid, v.resolve())
             leaf_cache[0], leaf_cache[1] = key, lv
             return lv
 
@@ -418,9 +457,11 @@ class GradientCommit:
             return comm.ulfm_collective(data)
 
         def on_failure(work: WorkResult) -> None:
-            nonlocal p_major, crossed, restore, t_fail
+            nonlocal p_major, crossed, restore, t_fail, reform_s
+            h0 = time.perf_counter()
             if t_fail is None:
-                t_fail = time.perf_counter()
+                t_fail = h0
+                self.mark("fail")
             rec = work.record
             # promoted spares admit the vacated replica's range (canonical R2)
             vacating = [r for r in sorted(rec.failed_replicas)
@@ -459,6 +500,7 @@ class GradientCommit:
                 "n_bdry": decision.n_bdry,
                 "promoted": [[r, ro.value] for r, ro in decision.promoted],
                 "epoch_after": rec.epoch_after})
+            reform_s += time.perf_counter() - h0
 
         def restoration() -> Optional[WorkResult]:
             nonlocal restore
@@ -520,6 +562,8 @@ class GradientCommit:
                 break
 
         self._end_of_step()
+        if t_fail is not None:
+            self.mark("commit")
         # ---- commit ----
         members = list(comm.members)
         reg, bdy = comm.census_contrib()
@@ -551,4 +595,5 @@ class GradientCommit:
             rounds=cnt["rounds"], passes=cnt["passes"], reduces=cnt["reduces"],
             rewinds=cnt["rewinds"], boundary_crossed=crossed,
             launches=cnt["launches"],
-            failure_wall_s=(time.perf_counter() - t_fail) if t_fail else None)
+            failure_wall_s=(time.perf_counter() - t_fail) if t_fail else None,
+            reform_host_s=reform_s)

@@ -50,6 +50,11 @@
 static thread_local std::string g_err;
 static std::atomic<unsigned long long> g_launches{0};  // kernels launched by this library
 
+extern "C" int rcv_set_error(int code, const char *msg) {
+  g_err = msg;
+  return code;
+}
+
 static int set_err(int code, const char *fmt, ...) {
   char buf[512];
   va_list ap;
@@ -355,6 +360,38 @@ template <int L> struct ProgFull {
   }
 };
 
+// A fixed canonical-tree program known at compile time (a degraded cover of
+// the multi-process combine, tools/cover_shapes.py -> shapes.inc): input i is
+// pushed, then the top two stack entries merge OPS[i] times (3 bits per
+// input).  Every stack index is a template constant, so the evaluation is
+// straight-line code over registers, like ProgFull, instead of ProgTree's
+// parameter-driven walk over 2^(L+1)-1 heap nodes.
+template <int N, unsigned long long OPS> struct ProgFixed {
+  template <int SP, int M, typename V>
+  __device__ __forceinline__ static void merge(V (&s)[N]) {
+    if constexpr (M > 0) {
+      s[SP - 2] = vadd(s[SP - 2], s[SP - 1]);
+      merge<SP - 1, M - 1>(s);
+    }
+  }
+  template <int I, int SP, typename V, typename Ld>
+  __device__ __forceinline__ static void push(V (&s)[N], const Ld &ld) {
+    if constexpr (I < N) {
+      constexpr int M = (int)((OPS >> (3 * I)) & 7ull);
+      static_assert(M <= SP, "fixed program merges below the stack");
+      s[SP] = ld(I);
+      merge<SP + 1, M>(s);
+      push<I + 1, SP + 1 - M>(s, ld);
+    }
+  }
+  template <typename V, typename Ld, typename P = FoldParams>
+  __device__ __forceinline__ static V eval(const P &, const Ld &ld) {
+    V s[N];
+    push<0, 0>(s, ld);
+    return s[0];
+  }
+};
+
 // Several disjoint perfect subtrees in one pass (a rank's local cover after
 // a failure, e.g. 8 + 4 + 2 + 1 leaves): each root is stored to its own
 // output, without the divisor (pre-reduce partials).
@@ -423,12 +460,17 @@ __global__ void __launch_bounds__(256)
 // instead of 2^L (the loop body's stores otherwise fence the next loads).
 template <typename P> struct FullTree { static constexpr int value = -1; };
 template <int L> struct FullTree<ProgFull<L>> { static constexpr int value = L; };
+// inputs of a straight-line program (0: not straight-line)
+template <typename P> struct StraightIn { static constexpr int value = 0; };
+template <int L> struct StraightIn<ProgFull<L>> { static constexpr int value = 1 << L; };
+template <int N, unsigned long long OPS> struct StraightIn<ProgFixed<N, OPS>> {
+  static constexpr int value = N;
+};
 
 template <typename Prog>
 __global__ void __launch_bounds__(256)
     fold_direct_pair_kernel(const __grid_constant__ FoldParams p) {
-  constexpr int L = FullTree<Prog>::value;
-  constexpr int NIN = 1 << L;
+  constexpr int NIN = StraightIn<Prog>::value;
   if (p.guard && (*p.guard & p.guard_mask)) return;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   for (unsigned long long v = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -444,7 +486,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       if (u == 1 && !has_w) break;
-      float4 r = ProgFull<L>::template node<L, 0, float4>([&](int i) { return x[u][i]; });
+      float4 r = Prog::template eval<float4>(p, [&](int i) { return x[u][i]; });
       if (p.divisor != 0.0) r = vdiv(r, p.divisor);
       const unsigned long long off = (u ? w : v) * 16ull;
       for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + off, r);
@@ -637,6 +679,48 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
+// K-ACC: one carry-chain push of the canonical dyadic accumulator
+
+#define KACC_MAX_SEGS 256
+#define KACC_MAX_DEPTH 8
+
+struct KaccParams {
+  const char *src[KACC_MAX_SEGS];
+  unsigned long long off[KACC_MAX_SEGS + 1];  // flat element offsets, off[n_seg] = numel
+  const float *stack[KACC_MAX_DEPTH];         // [0] deepest merged node .. [c-1] top
+  float *out;
+  unsigned long long nvec;  // 4-element vectors
+  int n_seg;
+  int c;
+  int bf16;
+};
+
+__global__ void __launch_bounds__(256) kacc_kernel(const __grid_constant__ KaccParams p) {
+  for (unsigned long long v = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+       v < p.nvec; v += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long e = v * 4ull;
+    // segment holding e (warp-uniform almost everywhere: a warp covers 128
+    // contiguous elements and segments are whole parameter tensors)
+    int lo = 0, hi = p.n_seg - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (p.off[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    const unsigned long long r = e - p.off[lo];
+    float4 x = p.bf16 ? ld_vec<float>(p.src[lo] + r * 2ull, true)
+                      : ld_vec<float>(p.src[lo] + r * 4ull, false);
+    // canonical order: the new leaf is the right child of every node it
+    // completes, so it is added on the right, innermost (top) first
+    for (int i = p.c - 1; i >= 0; --i)
+      // coherent load: out may alias stack[0] (the merge is in place)
+      x = vadd(__ldcg(reinterpret_cast<const float4 *>(p.stack[i] + e)), x);
+    // c == 0: the leaf node itself, bit for bit (a -0.0 gradient stays -0.0,
+    // as in the fused commit's tree)
+    *reinterpret_cast<float4 *>(p.out + e) = x;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // small utility kernels
 
 __global__ void compare_kernel(const uint32_t *a, const uint32_t *b,
@@ -772,12 +856,15 @@ struct BarrierParams {
   int n_now, n_prev;
   unsigned long long now_value, prev_value;
   unsigned int *err;
+  // real-kill mode: the node's liveness dead word (mapped host memory,
+  // rcv_liveness); a peer whose bit is set is not waited for
+  const volatile unsigned int *host_dead;
 };
 
 __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   const int t = threadIdx.x;
   // a peer that already timed out is dead: never signal or wait on it again
-  const unsigned int dead = *(volatile const unsigned int *)p.status;
+  const unsigned int dead = *(volatile const unsigned int *)p.status | (p.host_dead ? *p.host_dead : 0u);
   const bool peer = t < p.n && t != p.me && ((p.live >> t) & 1ull) && !((dead >> t) & 1u);
   // everything this GPU wrote before this kernel (partials, remote stores)
   // is made visible system-wide before the flag store releases it
@@ -791,7 +878,7 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
     for (;;) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.local + t) : "memory");
       if (v >= p.value) break;
-      if (globaltimer() - t0 > p.timeout_ns) {
+      if (globaltimer() - t0 > p.timeout_ns || (p.host_dead && ((*p.host_dead >> t) & 1u))) {
         atomicOr(p.status, 1u << (t & 31));
         break;
       }
@@ -861,6 +948,7 @@ struct FoldReq {
   // halves the per-byte cost of a branchy evaluator's control flow
   bool wide32 = false;
   bool pair = false;  // DIRECT: two vectors per thread (small perfect trees, fp32)
+  int shape = -1;     // >= 0: index of a compile-time program (shapes.inc)
 };
 
 enum { PK_STACK = 0, PK_LEFT = 1, PK_TREE = 2 };
@@ -957,8 +1045,8 @@ int launch_direct_p(const FoldReq &r, unsigned long long e0, unsigned long long 
   unsigned long long blocks = std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)sms * 8));
   if (r.max_ctas > 0) blocks = std::min<unsigned long long>(blocks, (unsigned long long)r.max_ctas * 4);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  if constexpr (std::is_same<A, float>::value && FullTree<Prog>::value >= 0 &&
-                FullTree<Prog>::value <= 3) {
+  if constexpr (std::is_same<A, float>::value && StraightIn<Prog>::value >= 1 &&
+                StraightIn<Prog>::value <= 16) {
     if (r.pair) {
       // the same (SM-share-capped) grid: twice the bytes in flight per SM
       fold_direct_pair_kernel<Prog><<<(unsigned)blocks, 256, 0, st>>>(p);
@@ -1041,6 +1129,25 @@ int launch_tma_p(const FoldReq &r, const TmaGeom &g, unsigned long long e0,
   return RCV_OK;
 }
 
+// Straight-line evaluators of the degraded covers (shapes.inc), DIRECT only.
+template <typename A>
+int launch_shape(const FoldReq &r, unsigned long long e0, unsigned long long nvec,
+                 cudaStream_t st, int sms) {
+  if constexpr (std::is_same<A, double>::value) {
+    return set_err(RCV_EINVAL, "fixed tree programs are fp32 only");
+  } else {
+    switch (r.shape) {
+#define RCV_SHAPE(I, N, OPS) \
+  case I:                    \
+    return launch_direct_p<A, ProgFixed<N, OPS>>(r, e0, nvec, st, sms);
+#include "shapes.inc"
+#undef RCV_SHAPE
+      default:
+        return set_err(RCV_EINVAL, "unknown fixed tree program %d", r.shape);
+    }
+  }
+}
+
 // Launch `variant` (TMA / DIRECT) of the best program policy for r.
 template <typename A>
 int launch_vec(const FoldReq &r, bool tma, const TmaGeom &g, int maxd,
@@ -1048,6 +1155,8 @@ int launch_vec(const FoldReq &r, bool tma, const TmaGeom &g, int maxd,
 #define RCV_LAUNCH(PROG) \
   return tma ? launch_tma_p<A, PROG>(r, g, e0, nvec, st, sms) : launch_direct_p<A, PROG>(r, e0, nvec, st, sms)
   if (r.n_roots > 0) RCV_LAUNCH(ProgForest);
+  if (r.shape >= 0 && !tma && !std::is_same<A, double>::value)
+    return launch_shape<A>(r, e0, nvec, st, sms);
   if (r.full_L >= 0 && r.full_L <= 6) {
     switch (r.full_L) {
       case 0: RCV_LAUNCH(ProgFull<0>);
@@ -1126,7 +1235,8 @@ int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int s
     // LDG.128 (93% of HBM at N=1 vs 87% through the TMA ring); evaluators
     // with warp-uniform branches (ProgTree, ProgStack, ProgLeft) keep the TMA
     // ring, which decouples their loads from the control flow.
-    if (variant == RCV_VARIANT_AUTO && (r.full_L >= 0 || r.n_roots > 0)) variant = RCV_VARIANT_DIRECT;
+    if (variant == RCV_VARIANT_AUTO && (r.full_L >= 0 || r.n_roots > 0 || r.shape >= 0))
+      variant = RCV_VARIANT_DIRECT;
     bool use_tma = variant == RCV_VARIANT_TMA || variant == RCV_VARIANT_AUTO;
     const bool geom_ok = f64 ? tma_geom<double>(r, &g) : (wide ? tma_geom<F8>(r, &g) : tma_geom<float>(r, &g));
     if (use_tma && !geom_ok) {
@@ -1362,6 +1472,48 @@ int rcv_accumulate(void *acc, const void *grad, int acc_dtype, int grad_dtype,
   return run_fold(r, numel, RCV_VARIANT_AUTO, (cudaStream_t)stream, current_device_sms());
 }
 
+int rcv_kacc_push(const void *const *seg_ptr, const uint64_t *seg_off, const uint64_t *seg_len,
+                  int n_seg, int grad_dtype, const float *const *stack, int c, float *out,
+                  size_t numel, void *stream) {
+  if (n_seg < 1 || n_seg > KACC_MAX_SEGS) return set_err(RCV_ERANGE, "kacc: %d segments (1..%d)", n_seg, KACC_MAX_SEGS);
+  if (c < 0 || c > KACC_MAX_DEPTH) return set_err(RCV_ERANGE, "kacc: carry chain %d (0..%d)", c, KACC_MAX_DEPTH);
+  if (grad_dtype != RCV_F32 && grad_dtype != RCV_BF16) return set_err(RCV_EINVAL, "kacc: gradient dtype %d", grad_dtype);
+  if (!out || ((uintptr_t)out & 15)) return set_err(RCV_EINVAL, "kacc: output must be 16-byte aligned");
+  KaccParams p;
+  memset(&p, 0, sizeof p);
+  unsigned long long pos = 0;
+  const unsigned align = grad_dtype == RCV_BF16 ? 8u : 16u;
+  for (int i = 0; i < n_seg; ++i) {
+    if (seg_off[i] != pos) return set_err(RCV_EINVAL, "kacc: segment %d starts at %llu, want %llu", i,
+                                          (unsigned long long)seg_off[i], pos);
+    if (seg_len[i] % 4 || ((uintptr_t)seg_ptr[i] & (align - 1)))
+      return set_err(RCV_EINVAL, "kacc: segment %d (%llu elements at %p) is not a whole, aligned "
+                     "number of 4-element vectors", i, (unsigned long long)seg_len[i], seg_ptr[i]);
+    p.src[i] = (const char *)seg_ptr[i];
+    p.off[i] = pos;
+    pos += seg_len[i];
+  }
+  if (pos != numel) return set_err(RCV_EINVAL, "kacc: segments hold %llu elements, want %zu", pos, numel);
+  p.off[n_seg] = pos;
+  for (int i = 0; i < c; ++i) {
+    if (!stack[i] || ((uintptr_t)stack[i] & 15)) return set_err(RCV_EINVAL, "kacc: stack entry %d must be 16-byte aligned", i);
+    p.stack[i] = stack[i];
+  }
+  p.out = out;
+  p.nvec = numel / 4;
+  p.n_seg = n_seg;
+  p.c = c;
+  p.bf16 = grad_dtype == RCV_BF16;
+  if (!p.nvec) return RCV_OK;
+  const int sms = current_device_sms();
+  const unsigned long long blocks = std::max<unsigned long long>(
+      1, std::min<unsigned long long>((p.nvec + 255) / 256, (unsigned long long)sms * 8));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  kacc_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(p);
+  CK(cudaGetLastError());
+  return RCV_OK;
+}
+
 int rcv_tree_program(const uint32_t *lo, const uint32_t *level, int n_blocks,
                      uint32_t n_leaves, uint8_t *ops_out, int *max_depth) {
   if (n_blocks < 0 || n_blocks > RCV_MAX_IN) return set_err(RCV_ERANGE, "block count %d out of range", n_blocks);
@@ -1466,6 +1618,25 @@ int prepare_tree(const rcv_block *blocks, int n_blocks, uint32_t n_leaves, int n
       while ((1 << fl) < n_blocks) ++fl;
       r.full_L = fl;
     }
+  }
+  if (r.full_L < 0 && acc_dtype == RCV_F32 && n_blocks <= 21 && !getenv("RCV_NO_FIXED")) {
+    // a compile-time program for this cover (the degraded combines)?
+    static const struct {
+      int n;
+      unsigned long long ops;
+    } kShapes[] = {
+#define RCV_SHAPE(I, N, OPS) {N, OPS},
+#include "shapes.inc"
+#undef RCV_SHAPE
+    };
+    unsigned long long packed = 0;
+    bool fits = true;
+    for (int i = 0; i < n_blocks; ++i) {
+      fits &= (r.op[i] & RCV_OP_MERGES_MASK) <= 7;
+      packed |= (unsigned long long)(r.op[i] & 7) << (3 * i);
+    }
+    for (int s = 0; fits && s < (int)(sizeof kShapes / sizeof kShapes[0]); ++s)
+      if (kShapes[s].n == n_blocks && kShapes[s].ops == packed) r.shape = s;
   }
   return RCV_OK;
 }
@@ -2038,6 +2209,11 @@ int rcv_ctx_destroy(rcv_ctx *c) {
   return RCV_OK;
 }
 
+int rcv_ctx_set_liveness(rcv_ctx *c, const uint32_t *device_dead_word) {
+  c->bar.host_dead = (const volatile unsigned int *)device_dead_word;
+  return RCV_OK;
+}
+
 int rcv_ctx_set_timing(rcv_ctx *c, int on) {
   c->timing = on != 0;
   return RCV_OK;
@@ -2165,7 +2341,9 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
     p->comb.max_ctas = env_ctas("RCV_COMB_CTAS", ctx->sms, comb_share(d));
     // branchy trees (fragmented covers) evaluate 8-element vectors: half the
     // control flow per byte (N=2 degraded combine 167 -> 99 us)
-    p->comb.wide32 = p->comb.full_L < 0;
+    // (straight-line fixed programs keep 4-element vectors, two per thread,
+    // like the perfect trees; RCV_WIDE_FIXED=1 measures the alternative)
+    p->comb.wide32 = p->comb.full_L < 0 && (p->comb.shape < 0 || getenv("RCV_WIDE_FIXED"));
     // perfect trees over <= 8 nodes: two vectors per thread in flight
     p->comb.pair = true;
     if (d->guarded) {

@@ -45,7 +45,7 @@ import torch.distributed as dist
 
 from . import _lib
 from .comm import Communicator
-from .commit import GradientCommit, aligned_bounds, block_cover
+from .commit import GradientCommit, aligned_bounds, block_cover, input_nodes
 from .policy import assign_roles, initial_state, policy_advancement
 
 
@@ -126,11 +126,11 @@ class VmmBuffers:
         self.rank, self.world, self.group = rank, world, group
         self.timeout_s = timeout_s
         got = [None] * world
-        dist.all_gather_object(got, (os.getpid(), secrets.token_hex(16) if rank == 0 else None),
-                               group=group)
+        mine = (secrets.token_hex(4), secrets.token_hex(16)) if rank == 0 else None
+        dist.all_gather_object(got, (os.getpid(), mine), group=group)
         self.pids = {pid for pid, _ in got}
-        self.secret = got[0][1].encode()
-        self.job = self.secret[:8].decode()
+        self.job, secret = got[0][1]
+        self.secret = secret.encode()
         self.dev = torch.cuda.current_device()
         self._keep = []  # fds and tensors that must outlive the mappings
 
@@ -197,43 +197,69 @@ class VmmBuffers:
 
 class DeadPeerDetector:
     """Injector for real-kill mode on the survivors: they are not told the
-    schedule.  At a poll point (after_sync, once per iteration, and
-    before_sync of the next) it synchronises the device, reads the barrier
-    status word and reports every replica held by a rank whose barrier wait
-    timed out — the crash-stop detection of comm.py:129-172 driven by the
-    hardware instead of the simulator.  Optionally re-forms the torch
-    process group without the dead ranks (ncclCommShrink via
-    torch.distributed.shrink_group).
+    schedule; they find out, at the protocol's poll points, which ranks the
+    hardware saw die — the crash-stop detection and agreement of
+    comm.py:129-172 driven by the machine instead of the simulator.
 
-    per_bucket=True also polls before every bucket's collective
-    ("during_sync", the injection points of trainer.py:425), so a death is
-    detected one bucket after the barrier that timed out instead of at the
-    end of the cascade.  Each poll synchronises the device, which serialises
-    the bucket pipeline: it trades step time for detection latency."""
+    With the engine's node liveness (``rcv_liveness``: native heartbeats in
+    shared memory, a dead word every GPU's barrier kernel reads), a poll is
+    one host read and a compare-and-swap: poll point n of the replicated
+    control flow is decided by the first rank that reaches it, and every
+    survivor acts on that same failed set (``Liveness.decide``).  No device
+    synchronisation, so it polls before every bucket's collective
+    ("during_sync", trainer.py:425) as well as at before_sync / after_sync.
+
+    Without liveness it falls back to the barrier timeout: a poll
+    synchronises the device and reads the status word (only at
+    before/after_sync unless per_bucket=True, since each poll serialises
+    the bucket pipeline).
+
+    shrink=True re-forms the torch process group without the dead ranks
+    (ncclCommShrink via torch.distributed.shrink_group), timed."""
 
     def __init__(self, engine: "DistributedGradientCommit", inner=None, shrink: bool = False,
-                 per_bucket: bool = False):
+                 per_bucket: Optional[bool] = None):
         self.engine, self.inner, self.shrink = engine, inner, shrink
-        self.per_bucket = per_bucket
+        lv = getattr(engine, "liveness", None)
+        self.per_bucket = lv is not None if per_bucket is None else per_bucket
         self.known = 0
+        self.seq = 0
         self.detections: List[dict] = []
 
     def fire(self, phase, bucket=None):
+        import time
         out = list(self.inner.fire(phase, bucket)) if self.inner is not None else []
         polls = ("after_sync", "before_sync", "during_sync") if self.per_bucket else \
             ("after_sync", "before_sync")
         if phase not in polls:
             return out
-        import time
         t0 = time.perf_counter()
-        torch.cuda.synchronize(self.engine.device)
-        bits = int(self.engine.status[0].item()) & ~self.known
+        lv = getattr(self.engine, "liveness", None)
+        rec = {}
+        if lv is not None:
+            self.seq += 1
+            mask, decided_ns = lv.decide(self.seq)
+            bits = mask & ~self.known
+            if bits:
+                rec["poll"] = self.seq
+                rec["decided_ns"] = decided_ns
+        else:
+            torch.cuda.synchronize(self.engine.device)
+            bits = int(self.engine.status[0].item()) & ~self.known
         if bits:
             self.known |= bits
             dead_ranks = [r for r in range(self.engine.world) if (bits >> r) & 1]
-            victims = [rid for rid in self.engine.comm.members if self.engine.rank_of[rid] in dead_ranks]
-            rec = {"phase": phase, "bucket": bucket, "ranks": dead_ranks, "replicas": victims,
-                   "sync_ms": (time.perf_counter() - t0) * 1e3}
+            victims = [rid for rid in self.engine.comm.members
+                       if self.engine.rank_of[rid] in dead_ranks]
+            rec.update(phase=phase, bucket=bucket, ranks=dead_ranks, replicas=victims,
+                       poll_ms=(time.perf_counter() - t0) * 1e3)
+            if lv is not None:
+                st = lv.stats(dead_ranks[0])
+                rec.update(dead_ns=st["dead_ns"], kill_ns=st["kill_ns"], seen_ns=st["now_ns"])
+                if st["kill_ns"] and st["dead_ns"]:
+                    rec["detect_ms"] = (st["dead_ns"] - st["kill_ns"]) / 1e6
+                if st["dead_ns"] and rec.get("decided_ns"):
+                    rec["agree_ms"] = max(0, rec["decided_ns"] - st["dead_ns"]) / 1e6
             if self.shrink and hasattr(dist, "shrink_group"):
                 t1 = time.perf_counter()
                 try:
@@ -247,23 +273,29 @@ class DeadPeerDetector:
 
 
 class RealKill:
-    """Victim-side injector: at (step, phase, bucket) this process drains its
-    own GPU work and dies by SIGKILL (the paper's failure simulator,
-    PAPER.md:715-726).  The drain makes sure no survivor is mid-read of
-    this rank's partials when the process disappears."""
+    """Victim-side injector: at (step, phase, bucket) this process dies by
+    SIGKILL (the paper's failure simulator) — at once, with
+    its queued and running kernels, unless drain_s > 0 asks it to finish its
+    GPU work first.  Survivors never read a dead rank's memory after the
+    agreed detection; what it left half-written before is re-reduced (every
+    bucket tagged before the failure is stale)."""
 
-    def __init__(self, step: int, phase: str, bucket=None, drain_s: float = 0.3):
+    def __init__(self, step: int, phase: str, bucket=None, drain_s: float = 0.0,
+                 liveness=None):
         self.at = (step, phase, bucket)
         self.step = -1
         self.drain_s = drain_s
+        self.liveness = liveness
 
     def fire(self, phase, bucket=None):
         if (self.step, phase, bucket if phase == "during_sync" else None) == self.at:
-            import os
             import signal
             import time
-            torch.cuda.synchronize()
-            time.sleep(self.drain_s)
+            if self.drain_s > 0:
+                torch.cuda.synchronize()
+                time.sleep(self.drain_s)
+            if self.liveness is not None:
+                self.liveness.note_kill()
             os.kill(os.getpid(), signal.SIGKILL)
         return []
 
@@ -279,7 +311,8 @@ class DistributedGradientCommit(GradientCommit):
                  variant: int = _lib.VARIANT_AUTO,
                  combine_variant: int = _lib.VARIANT_AUTO,
                  pool_slots: int = 8, barrier_timeout_s: float = 30.0,
-                 real_kill: bool = False):
+                 real_kill: bool = False, liveness_deadline_s: Optional[float] = 10e-3,
+                 liveness_period_s: float = 1e-3):
         if policy_kind not in ("static", "adaptive"):
             raise ValueError("unknown policy kind %r" % (policy_kind,))
         self.rank = dist.get_rank(group) if rank is None else rank
@@ -341,6 +374,19 @@ class DistributedGradientCommit(GradientCommit):
                          for r in members}
         self.rt = _lib.BucketRuntime(self.world, self.rank, self.flags, self.flag_ptr,
                                      self.status, self.timeout_ns)
+        self.liveness: Optional[_lib.Liveness] = None
+        if real_kill and liveness_deadline_s:
+            # node-local heartbeats: a dead peer is declared within the
+            # deadline and every barrier kernel stops waiting for it at once
+            self.liveness = _lib.Liveness("/rcv-live-%s" % vb.job, self.rank, self.world,
+                                          liveness_period_s, liveness_deadline_s)
+            dist.barrier(group=group)
+            if self.rank == 0:  # every rank has it mapped: drop the name
+                try:
+                    os.unlink("/dev/shm/rcv-live-%s" % vb.job)
+                except OSError:
+                    pass
+            self.rt.set_liveness(self.liveness)
         self._plan_key = None
         torch.cuda.synchronize(self.device)
         dist.barrier(group=group)
@@ -399,6 +445,9 @@ class DistributedGradientCommit(GradientCommit):
                 ranges[rid] = ids[rk][k:k + q]
                 k += q
         return ranges
+
+    def _stream_device(self) -> torch.device:
+        return self.device
 
     def _live_ranks(self) -> List[int]:
         return sorted({self.rank_of[r] for r in self.comm.members})
@@ -471,14 +520,15 @@ class DistributedGradientCommit(GradientCommit):
         owner = {m: self.rank_of[rid] for m, (rid, _) in leaves.items()}
         cover, slot_of = plan_bucket(owner, b, ranks, self.pool_slots)
         Block = _lib._Block
+        nodes = input_nodes({m: v for m, v in leaves.items() if v[1] is not None})
         pre_blocks, pre_counts, pre_leaves, pre_out = [], [], [], []
         for blo, blev in cover:
             rk, j = slot_of[(blo, blev)]
             if rk != self.rank:
                 continue
-            span = [m for m in sorted(leaves) if blo <= m < blo + (1 << blev)]
-            pre_blocks += [Block(leaves[m][1].data_ptr(), m - blo, 0,
-                                 _lib.dtype_code(leaves[m][1])) for m in span]
+            span = [n for n in nodes if blo <= n[0] < blo + (1 << blev)]
+            pre_blocks += [Block(t.data_ptr(), lo - blo, lev, _lib.dtype_code(t))
+                           for lo, lev, t in span]
             pre_counts.append(len(span))
             pre_leaves.append(1 << blev)
             pre_out.append(self.pool_ptr[self.rank] + j * self.lmax * self._es)

@@ -13,9 +13,18 @@ forward/backward, the loss and parameter trajectory under any failure
 schedule is then bitwise the failure-free one.
 
 Parameters live in one flat fp32 buffer (the module's parameters are views
-into it), each microbatch's gradient is written into its own flat slot (the
-commit's leaf), and the committed gradient buffer of replica 0 is the
-optimizer's gradient.
+into it) and the committed gradient buffer of replica 0 is the optimizer's
+gradient.  Microbatch gradients reach the commit one of two ways:
+
+* ``kacc=True`` (default): backward's per-parameter gradient tensors are
+  pushed, in place, into the replica's K-ACC stack (kacc.py): one launch per
+  microbatch merges the carry chain, nothing is copied into a flat buffer,
+  and a replica holds O(log G) gradient-sized nodes; the commit evaluates the
+  top of the canonical tree over the nodes;
+* ``kacc=False``: each microbatch gradient is copied into its own flat slot
+  (B slots resident) and the commit reads every slot.
+
+Both commit the same bits (the canonical tree depends only on the leaves).
 """
 
 from __future__ import annotations
@@ -25,6 +34,7 @@ from typing import Callable, Dict, List, Tuple
 import torch
 import torch.nn as nn
 
+from . import kacc as _kacc
 from .commit import CommitOutcome, GradientCommit
 
 
@@ -56,7 +66,8 @@ class CanonicalExecutor:
 
     def __init__(self, module: nn.Module, batch_fn: Callable, loss_fn: Callable,
                  w_init: int, g_init: int, k_buckets: int, lr: float = 0.05,
-                 device="cuda:0", spares: int = 0, policy_kind: str = "static"):
+                 device="cuda:0", spares: int = 0, policy_kind: str = "static",
+                 kacc: bool = True):
         self.device = torch.device(device)
         self.module = module.to(self.device)
         self.flat, self.params = flatten_module(self.module, self.device)
@@ -65,7 +76,16 @@ class CanonicalExecutor:
                                      placement={r: self.device for r in range(w_init + spares)},
                                      spares=spares, policy_kind=policy_kind)
         self.b = w_init * g_init
-        self.slots = torch.empty(self.b, self.numel, dtype=torch.float32, device=self.device)
+        self.g = g_init
+        self.kacc = kacc
+        if kacc:
+            bad = [tuple(p.shape) for p in self.params if p.numel() % 4]
+            if bad:
+                raise ValueError("K-ACC needs parameters of whole 4-element vectors: %s" % bad[:4])
+            self.pool = _kacc.SlotPool(self.numel, self.device)
+            self.accs = {r: _kacc.KAccumulator(self.pool) for r in range(w_init + spares)}
+        else:
+            self.slots = torch.empty(self.b, self.numel, dtype=torch.float32, device=self.device)
         self.batch_fn, self.loss_fn, self.lr = batch_fn, loss_fn, lr
         self.computed: List[Tuple[int, int, int]] = []  # (step, m, rid) forward/backward log
 
@@ -79,16 +99,33 @@ class CanonicalExecutor:
             off += n
         return loss.detach()
 
-    def step(self, t: int, injector=None) -> Tuple[CommitOutcome, float]:
-        done: Dict[int, Tuple[int, torch.Tensor]] = {}
-        losses: Dict[int, torch.Tensor] = {}
+    def memory_report(self) -> dict:
+        """K-ACC slot usage against the O(log G) bound (bytes per slot)."""
+        if not self.kacc:
+            return {"slot_bytes": self.numel * 4, "slots_allocated": self.b}
+        return _kacc.memory_report({self.device: self.pool}, self.accs, self.g, self.numel)
 
-        def leaf(m: int, rid: int) -> torch.Tensor:
+    def step(self, t: int, injector=None) -> Tuple[CommitOutcome, float]:
+        done: Dict[int, Tuple[int, object]] = {}
+        losses: Dict[int, torch.Tensor] = {}
+        if self.kacc:
+            for acc in self.accs.values():
+                acc.reset()
+
+        def leaf(m: int, rid: int):
             # a microbatch is computed once by the replica that admits it; a
             # survivor that takes over a dead replica's index recomputes it
             if m not in done or done[m][0] != rid:
-                losses[m] = self._grad_into(self.slots[m], self.batch_fn(t, m))
-                done[m] = (rid, self.slots[m])
+                batch = self.batch_fn(t, m)
+                if self.kacc:
+                    loss = self.loss_fn(self.module, batch)
+                    grads = torch.autograd.grad(loss, self.params)
+                    self.accs[rid].push(m, [g.reshape(-1) for g in grads])
+                    losses[m] = loss.detach()
+                    done[m] = (rid, _kacc.Pending(self.accs[rid], m))
+                else:
+                    losses[m] = self._grad_into(self.slots[m], batch)
+                    done[m] = (rid, self.slots[m])
                 self.computed.append((t, m, rid))
             return done[m][1]
 

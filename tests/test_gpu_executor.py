@@ -26,12 +26,12 @@ class Schedule:
         return [r for e in hit for r in e[2]]
 
 
-def train(w, g, k, steps, plan=None, seed=0):
+def train(w, g, k, steps, plan=None, seed=0, kacc=True):
     torch.use_deterministic_algorithms(True)
     torch.manual_seed(seed)
     model = TinyTransformer(layers=2, d=64, heads=4, seq=32)
     ex = CanonicalExecutor(model, synthetic_lm_batch(seed, micro=2, seq=32), lm_loss,
-                           w, g, k, lr=0.1)
+                           w, g, k, lr=0.1, kacc=kacc)
     sched = Schedule(plan or {})
     losses, outs = [], []
     for t in range(steps):
@@ -68,3 +68,17 @@ def test_successive_failures_8_to_4_bitwise():
     assert torch.equal(ref_p, p)
     assert outs[-1].w_cur == 4
     assert all(o.contrib_total == 32 for o in outs)
+
+
+def test_kacc_and_slots_commit_the_same_trajectory():
+    """K-ACC (backward's gradients pushed in place onto O(log G) stacks) and
+    per-microbatch slots (every gradient resident) commit the same bits,
+    with a failure; K-ACC holds at most log2(G)+2 slots per replica."""
+    plan = {1: [("during_sync", 1, [2])]}
+    l_s, p_s, _, _ = train(4, 8, 3, 3, plan, kacc=False)
+    l_k, p_k, _, ex = train(4, 8, 3, 3, plan, kacc=True)
+    assert l_s == l_k
+    assert torch.equal(p_s, p_k)
+    mem = ex.memory_report()
+    assert mem["peak_stack_depth_per_replica"] <= mem["bound_per_replica"]
+    assert mem["slots_allocated"] < mem["fused_design_slots"]

@@ -295,3 +295,28 @@ def test_random_stack_programs(variant, dtype):
         out = torch.empty(numel, dtype=dtype, device=DEV)
         _lib.fold([dev(x) for x in xs], ops, [out], divisor=div, variant=variant)
         assert host(out).tobytes() == want.tobytes(), (variant, trial, ops)
+
+
+def test_fixed_programs_of_degraded_covers():
+    """Every degraded combine cover of configs[1]'s group (shapes.inc, from
+    tools/cover_shapes.py) runs a compile-time straight-line evaluator; its
+    result is bitwise the oracle tree, on sizes with ragged heads and tails."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "cover_shapes.json")) as f:
+        shapes = json.load(f)
+    assert shapes
+    rng = np.random.default_rng(11)
+    for sh in shapes:
+        blocks = [tuple(b) for b in sh["cover"]]
+        ops, _ = _lib.tree_program(blocks, sh["n_leaves"])
+        assert list(ops) == sh["ops"]
+        for numel in (64 * 37, 64 * 37 + 5, 3):
+            vals = [rng.standard_normal(numel).astype(np.float32) for _ in blocks]
+            want = fold.tree_from_blocks([(v, lo, lev) for v, (lo, lev) in zip(vals, blocks)],
+                                         sh["n_leaves"]) / np.float32(sh["n_leaves"])
+            outs = [torch.empty(numel, dtype=torch.float32, device=DEV) for _ in range(2)]
+            _lib.tree_commit([(dev(v), lo, lev) for v, (lo, lev) in zip(vals, blocks)],
+                             sh["n_leaves"], outs, float(sh["n_leaves"]))
+            for o in outs:
+                assert host(o).tobytes() == want.tobytes(), (sh, numel)

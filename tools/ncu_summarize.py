@@ -66,5 +66,40 @@ def full(path):
                 print("raw | %s | %s | %s" % (name, units[i], vals[i]))
 
 
+_UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+
+
+def traffic(path, out="profiles/ncu_traffic.json", source=None):
+    """Merge the per-launch DRAM bytes of every kernel in a --set full report
+    into profiles/ncu_traffic.json (read by bench.py's roofline.traffic)."""
+    import json
+    import re
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"],
+                         check=True, capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    head, units = rr[0], rr[1]
+    try:
+        with open(out) as f:
+            doc = json.load(f)
+    except (OSError, ValueError):
+        doc = {"kernels": {}}
+    for vals in rr[2:]:
+        name = vals[head.index("Kernel Name")]
+        # template arguments as the bench names them: drop the `void ` and
+        # the parameter list
+        key = re.sub(r"^void ", "", name)
+        key = re.sub(r"\((FoldParams|BarrierParams)\)$", "", key).replace(" >", ">")
+        b = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = head.index(m)
+            b += float(vals[i].replace(",", "")) * _UNIT.get(units[i], 1.0)
+        t = head.index("gpu__time_duration.sum")
+        doc["kernels"][key] = {"dram_bytes": b, "duration": vals[t], "duration_unit": units[t],
+                               "report": source or path}
+    with open(out, "w") as f:
+        json.dump(doc, f, indent=1, sort_keys=True)
+    print(json.dumps(doc["kernels"], indent=1))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
