@@ -863,6 +863,15 @@ struct BarrierParams {
 
 __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   const int t = threadIdx.x;
+  // the previous combine on this stream has finished (kernel order): its
+  // producers' stamps must still be that call's.  Checked before this rank
+  // signals: no producer may rewrite that pool set before it has seen this
+  // rank arrive here, so a changed stamp means a real overwrite race.
+  if (t < p.n_prev) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.chk_prev[t]) : "memory");
+    if (v != p.prev_value) atomicOr(p.err, 2u);
+  }
   // a peer that already timed out is dead: never signal or wait on it again
   const unsigned int dead = *(volatile const unsigned int *)p.status | (p.host_dead ? *p.host_dead : 0u);
   const bool peer = t < p.n && t != p.me && ((p.live >> t) & 1ull) && !((dead >> t) & 1u);
@@ -886,16 +895,12 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   }
   __syncthreads();
   __threadfence_system();
-  if (t < p.n_prev || t < p.n_now) {
+  // every live peer has arrived, so every producer finished this call's
+  // partials: the stamps the combine behind this barrier reads must be set
+  if (t < p.n_now) {
     unsigned long long v;
-    if (t < p.n_prev) {
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.chk_prev[t]) : "memory");
-      if (v != p.prev_value) atomicOr(p.err, 2u);
-    }
-    if (t < p.n_now) {
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.chk_now[t]) : "memory");
-      if (v != p.now_value) atomicOr(p.err, 1u);
-    }
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.chk_now[t]) : "memory");
+    if (v != p.now_value) atomicOr(p.err, 1u);
   }
 }
 
@@ -1396,36 +1401,92 @@ int rcv_masked_allreduce(void *const *views, int n, uint64_t contrib_mask,
   return run_fold(r, numel, RCV_VARIANT_AUTO, (cudaStream_t)stream, current_device_sms());
 }
 
+}  // extern "C"
+
+namespace {
+// Flag arrays of one single-process device set (the drop-in multi-device
+// collective): 64 u64 barrier slots and a status word per device, allocated
+// once, read and written by peers over NVLink.
+struct MdGroup {
+  std::vector<int> devs;
+  std::vector<unsigned long long *> flags;
+  std::vector<unsigned int *> status;
+  unsigned long long seq = 0;
+};
+std::mutex g_md_mu;
+std::vector<MdGroup *> g_md;
+
+int md_group(const int *devices, int n, MdGroup **out) {
+  std::lock_guard<std::mutex> lk(g_md_mu);
+  for (MdGroup *g : g_md)
+    if ((int)g->devs.size() == n && std::equal(g->devs.begin(), g->devs.end(), devices)) {
+      *out = g;
+      return RCV_OK;
+    }
+  MdGroup *g = new MdGroup();
+  for (int d = 0; d < n; ++d) {
+    CK(cudaSetDevice(devices[d]));
+    unsigned long long *f = nullptr;
+    unsigned int *s = nullptr;
+    CK(cudaMalloc(&f, 64 * sizeof(unsigned long long)));
+    CK(cudaMemset(f, 0, 64 * sizeof(unsigned long long)));
+    CK(cudaMalloc(&s, sizeof(unsigned int)));
+    CK(cudaMemset(s, 0, sizeof(unsigned int)));
+    g->devs.push_back(devices[d]);
+    g->flags.push_back(f);
+    g->status.push_back(s);
+  }
+  CK(cudaDeviceSynchronize());
+  g_md.push_back(g);
+  *out = g;
+  return RCV_OK;
+}
+
+int md_barrier(MdGroup *g, int d, cudaStream_t st, unsigned long long value) {
+  BarrierParams p;
+  memset(&p, 0, sizeof p);
+  const int n = (int)g->devs.size();
+  for (int r = 0; r < n; ++r) p.peer[r] = g->flags[r];
+  p.local = g->flags[d];
+  p.status = g->status[d];
+  p.live = n >= 64 ? ~0ull : ((1ull << n) - 1);
+  p.value = value;
+  p.timeout_ns = 10ull * 1000000000ull;
+  p.n = n;
+  p.me = d;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  barrier_kernel<<<1, 32, 0, st>>>(p);
+  CK(cudaGetLastError());
+  return RCV_OK;
+}
+}  // namespace
+
+extern "C" {
+
+// One owner slice per device, fenced on both sides by a device-side flag
+// barrier among the devices (no host round trip, no per-call events): the
+// entry barrier proves every device's prior stream work (the contributors'
+// accumulation into their views) is done before any peer reads it, the exit
+// barrier that every remote store into this device's views has landed
+// before its stream moves on.
 int rcv_masked_allreduce_multidev(void *const *views, int n,
                                   uint64_t contrib_mask, int dtype,
                                   size_t numel, double divisor, int n_dev,
                                   const int *devices, void *const *streams) {
-  if (n_dev < 1 || n_dev > 64) return set_err(RCV_ERANGE, "device count %d out of range", n_dev);
+  if (n_dev < 1 || n_dev > 32) return set_err(RCV_ERANGE, "device count %d out of range", n_dev);
   FoldReq r;
   int rc = build_allreduce(r, views, n, contrib_mask, dtype, divisor);
   if (rc) return rc;
   if (numel == 0) return RCV_OK;
   int prev = 0;
   CK(cudaGetDevice(&prev));
-  // entry: every device's stream waits for every other stream's prior work
-  // (the contributors' accumulation), exit: likewise for the peers' stores.
-  std::vector<cudaEvent_t> ev(n_dev);
-  auto cross_order = [&]() -> int {
-    for (int d = 0; d < n_dev; ++d) {
-      CK(cudaSetDevice(devices[d]));
-      CK(cudaEventCreateWithFlags(&ev[d], cudaEventDisableTiming));
-      CK(cudaEventRecord(ev[d], (cudaStream_t)streams[d]));
-    }
-    for (int d = 0; d < n_dev; ++d) {
-      CK(cudaSetDevice(devices[d]));
-      for (int o = 0; o < n_dev; ++o)
-        if (o != d) CK(cudaStreamWaitEvent((cudaStream_t)streams[d], ev[o], 0));
-    }
-    for (int d = 0; d < n_dev; ++d) CK(cudaEventDestroy(ev[d]));
-    return RCV_OK;
-  };
-  rc = cross_order();
-  if (rc) return rc;
+  MdGroup *g = nullptr;
+  if ((rc = md_group(devices, n_dev, &g))) return rc;
+  const unsigned long long v_in = ++g->seq, v_out = ++g->seq;
+  for (int d = 0; d < n_dev; ++d) {
+    CK(cudaSetDevice(devices[d]));
+    if ((rc = md_barrier(g, d, (cudaStream_t)streams[d], v_in))) return rc;
+  }
   // owner slices, multiples of 8 elements (16-byte units for f32/f64 and bf16)
   const size_t unit = 8;
   const size_t units = (numel + unit - 1) / unit;
@@ -1441,8 +1502,10 @@ int rcv_masked_allreduce_multidev(void *const *views, int n,
     rc = run_fold(s, b - a, RCV_VARIANT_AUTO, (cudaStream_t)streams[d], dev_sms(devices[d]));
     if (rc) return rc;
   }
-  rc = cross_order();
-  if (rc) return rc;
+  for (int d = 0; d < n_dev; ++d) {
+    CK(cudaSetDevice(devices[d]));
+    if ((rc = md_barrier(g, d, (cudaStream_t)streams[d], v_out))) return rc;
+  }
   CK(cudaSetDevice(prev));
   return RCV_OK;
 }

@@ -60,20 +60,25 @@ def worker(rank, world, trials, seed, sizes):
         eng = DistributedGradientCommit(numel, world, g, k, barrier_timeout_s=60.0)
         bad_steps, err = [], None
         t0 = time.perf_counter()
-        try:
-            for s, plan in enumerate(plans):
+        for s, plan in enumerate(plans):
+            # a step that raised has still run to its end on every rank:
+            # record the error and keep the ranks in lockstep
+            try:
                 eng.step(s, lambda m, rid: dev[m], Kill(plan))
-                torch.cuda.synchronize()
-                bad = set()
-                for r in eng.comm.members:
-                    if eng._holds(r):
-                        got = eng.grads[r].cpu().numpy()
-                        bad |= {j for j, (lo, hi) in enumerate(eng.bounds)
-                                if got[lo:hi].tobytes() != want[lo:hi].tobytes()}
-                bad_steps.append(sorted(bad))
+            except CommitIntegrityError as exc:
+                err = err or str(exc)
+            torch.cuda.synchronize()
+            bad = set()
+            for r in eng.comm.members:
+                if eng._holds(r):
+                    got = eng.grads[r].cpu().numpy()
+                    bad |= {j for j, (lo, hi) in enumerate(eng.bounds)
+                            if got[lo:hi].tobytes() != want[lo:hi].tobytes()}
+            bad_steps.append(sorted(bad))
+        try:
             eng.check_peers()
         except CommitIntegrityError as exc:
-            err = str(exc)
+            err = err or str(exc)
         out.append(dict(trial=t, numel=numel, victim=victim, phase=phase, bucket=bucket,
                         bad=bad_steps, status=eng.status.tolist(), error=err,
                         ms=(time.perf_counter() - t0) * 1e3))

@@ -10,7 +10,11 @@ Times are CUDA events on every involved device (max), after warm-up; inputs
 are refreshed from a pristine copy before each timed call so every call
 reduces the same data.  algBW = S / t; busBW = 2 (live-1)/live * S / t
 (nccl-tests convention).  The reference fold (numpy, one thread, as shipped)
-is timed on the same shapes up to --cpu-max-mb.  One JSON line per case.
+is timed on the same shapes up to --cpu-max-mb.  When every replica has its
+own GPU, NCCL's (unmasked) all_reduce over the same device set
+(torch.cuda.nccl, single process) is timed at every size in the same file
+(impl "nccl").  A case with one live member reduces nothing: it is reported
+as a no-op, without bandwidths.  One JSON line per case.
 """
 
 import argparse
@@ -46,6 +50,26 @@ def time_reduce(comm_factory, views, pristine, devices, reps):
     return min(once() for _ in range(reps))
 
 
+def time_nccl(tensors, devices, reps):
+    """torch.cuda.nccl.all_reduce (sum, in place) over one tensor per GPU."""
+    import torch.cuda.nccl as nccl
+
+    def once():
+        evs = {d: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for d in devices}
+        for d in devices:
+            evs[d][0].record(torch.cuda.current_stream(d))
+        nccl.all_reduce(tensors)
+        for d in devices:
+            evs[d][1].record(torch.cuda.current_stream(d))
+        for d in devices:
+            torch.cuda.synchronize(d)
+        return max(a.elapsed_time(z) for a, z in evs.values())
+    for _ in range(3):
+        once()
+    return min(once() for _ in range(reps))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes-mb", default="1,4,16,64,256,1024")
@@ -64,6 +88,15 @@ def main():
             pristine = [torch.randn(numel, generator=torch.Generator().manual_seed(1234 + r)).to(devices[r])
                         for r in range(n)]
             views = {r: torch.empty_like(pristine[r]) for r in range(n)}
+            if n <= n_gpu:
+                ms = time_nccl([views[r] for r in range(n)], devices, args.reps)
+                s = numel * 4
+                rec = {"config": "configs[2]", "impl": "nccl", "bytes": s, "n": n, "dead": [],
+                       "live": n, "gpus": n, "ms": ms, "algbw_gbs": s / ms / 1e6,
+                       "busbw_gbs": 2 * (n - 1) / n * s / ms / 1e6,
+                       "note": "unmasked sum, NCCL's own order"}
+                print(json.dumps(rec), flush=True)
+                lines.append(rec)
             for dead in range(0, min(4, n)):
                 for pick in (("highest", list(range(n - dead, n))),
                              ("random", sorted(rng.sample(range(n), dead)))):
@@ -80,11 +113,15 @@ def main():
                                          sorted({devices[r] for r in live}, key=lambda d: d.index),
                                          args.reps)
                         s = numel * 4
-                        rec = {"config": "configs[2]", "bytes": s, "n": n, "dead": pick[1],
-                               "dead_pick": pick[0], "live": len(live), "spares": spare,
-                               "gpus": len({devices[r].index for r in live}),
-                               "ms": ms, "algbw_gbs": s / ms / 1e6,
-                               "busbw_gbs": 2 * (len(live) - 1) / len(live) * s / ms / 1e6}
+                        rec = {"config": "configs[2]", "impl": "ours", "bytes": s, "n": n,
+                               "dead": pick[1], "dead_pick": pick[0], "live": len(live),
+                               "spares": spare, "gpus": len({devices[r].index for r in live}),
+                               "ms": ms}
+                        if len(live) > 1:
+                            rec["algbw_gbs"] = s / ms / 1e6
+                            rec["busbw_gbs"] = 2 * (len(live) - 1) / len(live) * s / ms / 1e6
+                        else:
+                            rec["no_op"] = "one live member: nothing to reduce or send"
                         if mb <= args.cpu_max_mb and spare == 0 and pick[0] == "highest":
                             # the reference's fold as shipped: numpy, one thread
                             arrs = [pristine[r].cpu().numpy() for r in live]
