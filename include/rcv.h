@@ -282,6 +282,11 @@ int rcv_ctx_destroy(rcv_ctx *ctx);
 int rcv_ctx_finish(rcv_ctx *ctx, uint64_t live_mask, int participate,
                    void *main_stream);
 int rcv_ctx_set_timing(rcv_ctx *ctx, int on);
+/* A barrier over live_mask on main_stream behind everything this context
+ * enqueued (side and broadcast streams joined), outside the bucket sequence:
+ * the real-kill protocol's synchronisation point before it decides a step
+ * (a departed rank of the previous mask joins it, as for a bucket call). */
+int rcv_ctx_poll(rcv_ctx *ctx, uint64_t live_mask, int participate, void *main_stream);
 /* Real-kill mode: the node's liveness dead word (rcv_liveness_dead_word,
  * device pointer) that barrier kernels consult while they wait: a peer
  * declared dead is neither waited for nor signalled (status word 0 gets its

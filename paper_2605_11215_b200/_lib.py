@@ -32,7 +32,7 @@ EXPORTS = (
     "rcv_ipc_export", "rcv_ipc_import", "rcv_barrier", "rcv_tree_commit_at",
     "rcv_ctx_create", "rcv_ctx_destroy", "rcv_ctx_finish", "rcv_ctx_set_timing",
     "rcv_ctx_timing", "rcv_plan_create", "rcv_plan_destroy", "rcv_plan_bucket",
-    "rcv_vmm_alloc", "rcv_vmm_import", "rcv_kacc_push", "rcv_ctx_set_liveness",
+    "rcv_vmm_alloc", "rcv_vmm_import", "rcv_kacc_push", "rcv_ctx_set_liveness", "rcv_ctx_poll",
     "rcv_liveness_create", "rcv_liveness_dead_word", "rcv_liveness_decide",
     "rcv_liveness_stats", "rcv_liveness_note_kill", "rcv_liveness_destroy",
 )
@@ -132,6 +132,7 @@ def load() -> ctypes.CDLL:
         "rcv_kacc_push": (i32, [pvp, ctypes.POINTER(u64), ctypes.POINTER(u64), i32, i32,
                                 pvp, i32, vp, sz, vp]),
         "rcv_ctx_set_liveness": (i32, [vp, vp]),
+        "rcv_ctx_poll": (i32, [vp, u64, i32, vp]),
         "rcv_liveness_create": (i32, [ctypes.c_char_p, i32, i32, u64, u64, ctypes.POINTER(vp)]),
         "rcv_liveness_dead_word": (i32, [vp, ctypes.POINTER(vp), ctypes.POINTER(u32)]),
         "rcv_liveness_decide": (i32, [vp, u64, ctypes.POINTER(u32), ctypes.POINTER(u64)]),
@@ -482,6 +483,9 @@ class BucketRuntime:
 
     def finish(self, live_mask: int, participate: bool, stream: int) -> None:
         _check(load().rcv_ctx_finish(self.ctx, live_mask, int(participate), stream))
+
+    def poll(self, live_mask: int, participate: bool, stream: int) -> None:
+        _check(load().rcv_ctx_poll(self.ctx, live_mask, int(participate), stream))
 
     def set_timing(self, on: bool) -> None:
         _check(load().rcv_ctx_set_timing(self.ctx, int(on)))

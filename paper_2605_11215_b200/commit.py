@@ -204,6 +204,10 @@ class GradientCommit:
     def _end_of_step(self) -> None:
         """Hook run after the last bucket of a step is committed."""
 
+    def _sync_point(self, phase: str) -> None:
+        """Hook run before the injector's poll at `phase` (the multi-process
+        real-kill engine synchronises its data plane before after_sync)."""
+
     def _stream_device(self) -> torch.device:
         """Device whose current stream carries the commit's tail."""
         return self.placement[self.comm.members[0]] if self.comm.members else \
@@ -338,7 +342,11 @@ class GradientCommit:
         inj = injector if injector is not None else NullInjector()
         comm, state, b = self.comm, self.state, self.state.b
 
+        ver = [0]  # bumped whenever admissions, roles or membership change
+
         def kill(victims):
+            if victims:
+                ver[0] += 1
             for rid in victims:
                 if self.alive.get(rid):
                     self.alive[rid] = False
@@ -411,6 +419,7 @@ class GradientCommit:
                         provisional[rid].append(-1)   # nothing to shadow
                 elif j < len(ranges[rid]):
                     admitted[rid].append(ranges[rid][j])
+                    ver[0] += 1
                     comm.contrib_regular[rid] += 1
                 # else: executed and zeroed (trainer.py:229)
             elif rem_ext[rid] > 0:
@@ -418,15 +427,16 @@ class GradientCommit:
                 taken = {i for r in comm.members if r in admitted for i in admitted[r]}
                 nxt = next(i for i in range(b) if i not in taken)
                 admitted[rid].append(nxt)
+                ver[0] += 1
                 comm.contrib_boundary[rid] += 1
 
-        leaf_cache: list = [None, None]
+        leaf_cache: list = [None, None, None]
 
         def collect() -> Dict[int, Tuple[int, torch.Tensor]]:
             # the leaf set changes only when admissions, roles or membership
-            # do; reuse the dict (and with it the launch plan) otherwise
-            key = (comm.epoch, comm.boundary_latch,
-                   tuple((r, comm.roles[r], len(admitted.get(r, ()))) for r in comm.members))
+            # do (each bumps ver); reuse the dict (and with it the launch
+            # plan) otherwise
+            key = (comm.epoch, comm.boundary_latch, ver[0], len(comm.members))
             if leaf_cache[0] == key:
                 return leaf_cache[1]
             lv: Dict[int, Tuple[int, torch.Tensor]] = {}
@@ -440,7 +450,7 @@ class GradientCommit:
             for i, (rid, v) in lv.items():
                 if hasattr(v, "resolve"):
                     lv[i] = (rid, v.resolve())
-            leaf_cache[0], leaf_cache[1] = key, lv
+            leaf_cache[0], leaf_cache[1], leaf_cache[2] = key, lv, frozenset(lv)
             return lv
 
         committed_keys: Dict[int, frozenset] = {}
@@ -449,7 +459,7 @@ class GradientCommit:
         def reduce(k: int) -> WorkResult:
             def data():
                 lv = collect()
-                keys = frozenset(lv)
+                keys = leaf_cache[2]
                 if reuse and committed_keys.get(k) == keys:
                     return  # same index set, same leaf bits: already committed
                 cnt["launches"] += self._reduce_bucket(k, lv)
@@ -459,6 +469,7 @@ class GradientCommit:
         def on_failure(work: WorkResult) -> None:
             nonlocal p_major, crossed, restore, t_fail, reform_s
             h0 = time.perf_counter()
+            ver[0] += 1
             if t_fail is None:
                 t_fail = h0
                 self.mark("fail")
@@ -547,6 +558,7 @@ class GradientCommit:
                     on_failure(work)
             if not after_fired:
                 after_fired = True
+                self._sync_point(AFTER_SYNC)
                 kill(inj.fire(AFTER_SYNC))
             roles_before = dict(comm.roles)
             work = comm.ulfm_consensus()

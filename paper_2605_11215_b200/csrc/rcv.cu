@@ -1997,6 +1997,7 @@ struct rcv_ctx {
   // read this rank's pool sets and stored into its primary.
   uint64_t last_live = 0;
   WriteValue64 write_value = nullptr;  // cuStreamWriteValue64 (stamp_kernel when absent)
+  bool no_stamps = false;              // RCV_NO_STAMPS=1: measurement A/B only
   // the stamps the last combine on main read, re-checked by the next barrier
   std::vector<const unsigned long long *> chk;
   unsigned long long chk_value = 0;
@@ -2231,6 +2232,7 @@ int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer
   c->bar.n = n_ranks;
   c->bar.me = me;
   c->err = status + 1;
+  c->no_stamps = getenv("RCV_NO_STAMPS") && atoi(getenv("RCV_NO_STAMPS"));
   {
     // stream memory operations write the stamps without a kernel launch
     int ok = 0;
@@ -2325,6 +2327,21 @@ int rcv_ctx_finish(rcv_ctx *c, uint64_t live_mask, int participate, void *main_s
   c->in_step = false;
   c->last_live = 0;  // the closing barrier synchronised every live rank
   return RCV_OK;
+}
+
+int rcv_ctx_poll(rcv_ctx *c, uint64_t live_mask, int participate, void *main_stream) {
+  cudaStream_t st = (cudaStream_t)main_stream;
+  if (c->in_step) {
+    CK(cudaEventRecord(c->ev_ready, c->side));
+    CK(cudaStreamWaitEvent(st, c->ev_ready, 0));
+    if (c->bstream_dirty) {
+      CK(cudaEventRecord(c->ev_ready, c->bstream));
+      CK(cudaStreamWaitEvent(st, c->ev_ready, 0));
+    }
+  }
+  int rc = ctx_transition(c, live_mask, st);
+  if (rc) return rc;
+  return ctx_barrier(c, live_mask, participate != 0, st);
 }
 
 int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
@@ -2492,7 +2509,7 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
       if ((rc = ctx_flush(c, side, (long long)j - 3))) return rc;
     }
   }
-  const bool writes = p->participate && (p->has_forest || !p->pre.empty());
+  const bool writes = p->participate && (p->has_forest || !p->pre.empty()) && !c->no_stamps;
   if (writes && (rc = stamp_write(c, side, c->stamp_of(c->me, set), 0))) return rc;
   bool forest_done = false;
   if (p->has_forest && n % 64 == 0) {
@@ -2523,7 +2540,7 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
     const size_t units = (n + 63) / 64;
     a = std::min(n, p->slice_at(units, p->slice_q));
     z = std::min(n, p->slice_at(units, p->slice_q + 1));
-    if (z > a)
+    if (z > a && !c->no_stamps)
       for (int rk : p->producers) now.push_back(c->stamp_of(rk, set));
   }
   if ((rc = ctx_barrier(c, p->live_mask, p->participate, main, &now, j + 1))) return rc;

@@ -225,6 +225,7 @@ class DeadPeerDetector:
         self.known = 0
         self.seq = 0
         self.detections: List[dict] = []
+        self.shrinker = None
 
     def fire(self, phase, bucket=None):
         import time
@@ -261,12 +262,19 @@ class DeadPeerDetector:
                 if st["dead_ns"] and rec.get("decided_ns"):
                     rec["agree_ms"] = max(0, rec["decided_ns"] - st["dead_ns"]) / 1e6
             if self.shrink and hasattr(dist, "shrink_group"):
-                t1 = time.perf_counter()
-                try:
-                    dist.shrink_group(dead_ranks)
-                    rec["shrink_ms"] = (time.perf_counter() - t1) * 1e3
-                except Exception as exc:  # reported, not fatal: NCCL is off the data path
-                    rec["shrink_error"] = repr(exc)[:200]
+                # NCCL is off the commit's data path: re-form the torch group
+                # in the background, timed, while the step recovers
+                import threading
+
+                def shrink(rec=rec, ranks=list(dead_ranks)):
+                    t1 = time.perf_counter()
+                    try:
+                        dist.shrink_group(ranks)
+                        rec["shrink_ms"] = (time.perf_counter() - t1) * 1e3
+                    except Exception as exc:  # reported, not fatal
+                        rec["shrink_error"] = repr(exc)[:200]
+                self.shrinker = threading.Thread(target=shrink, daemon=True)
+                self.shrinker.start()
             self.detections.append(rec)
             out += victims
         return out
@@ -336,6 +344,7 @@ class DistributedGradientCommit(GradientCommit):
         self.device = torch.device("cuda", torch.cuda.current_device())
         self.placement = {r: self.device for r in members if self.rank_of[r] == self.rank}
         self.timing: Optional[list] = None
+        self.recovery_events: Optional[list] = None
         self._code = {torch.float32: _lib.F32, torch.float64: _lib.F64}[dtype]
         self._es = torch.tensor([], dtype=dtype).element_size()
 
@@ -462,6 +471,21 @@ class DistributedGradientCommit(GradientCommit):
         for r in ranks:
             mask |= 1 << r
         return ranks, mask
+
+    def _sync_point(self, phase: str) -> None:
+        """Real-kill mode, before the after_sync poll: one barrier over the
+        live ranks behind the step's last combine, then wait for the device.
+        A rank that died with this step's data plane in flight is then seen
+        dead by every survivor's device (liveness word or timeout) before the
+        protocol decides the step, so its death is decided here at the
+        latest and every bucket reduced before it is re-reduced (stale);
+        a death the protocol has not decided by now cannot have touched this
+        step's data (the rank arrived here after its last combine)."""
+        if not self.real_kill or phase != "after_sync":
+            return
+        ranks, mask = self._live_mask()
+        self.rt.poll(mask, self.rank in ranks, torch.cuda.current_stream(self.device).cuda_stream)
+        torch.cuda.synchronize(self.device)
 
     def _end_of_step(self) -> None:
         ranks, mask = self._live_mask()

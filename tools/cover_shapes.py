@@ -48,6 +48,7 @@ class HostSim(DistributedGradientCommit):
         self.pool_slots = 8
         self.shapes = set()
         self.examples = {}
+        self.step_t, self.phase = -1, ""
 
     def _holds(self, rid):
         return True
@@ -57,11 +58,19 @@ class HostSim(DistributedGradientCommit):
             return 0
         ranks = sorted({self.rank_of[r] for r in self.comm.members})
         owner = {m: self.rank_of[rid] for m, (rid, _) in leaves.items()}
-        cover, _ = plan_bucket(owner, self.state.b, ranks, self.pool_slots)
+        cover, slot_of = plan_bucket(owner, self.state.b, ranks, self.pool_slots)
         if not _perfect(cover, self.state.b):
             ops, _ = _lib.tree_program(cover, self.state.b)
-            self.shapes.add((len(cover), tuple(ops)))
-            self.examples.setdefault((len(cover), tuple(ops)), (self.state.b, list(cover)))
+            key = (len(cover), tuple(ops))
+            self.shapes.add(key)
+            self.examples.setdefault(key, (self.state.b, list(cover),
+                                           [ranks.index(slot_of[c][0]) for c in cover],
+                                           self.world, self.step_t, self.phase))
+        return 1
+
+    def step(self, t, leaf, injector=None):
+        self.step_t = t
+        return super().step(t, leaf, injector)
         return 1
 
     def _end_of_step(self):
@@ -133,8 +142,8 @@ def main():
             f.write("RCV_SHAPE(%d, %d, 0x%xull)  // %s\n" % (i, n, packed, list(ops)))
     import json
     with open(os.path.join(ROOT, "tests", "golden", "cover_shapes.json"), "w") as f:
-        json.dump([{"n_leaves": examples[s][0], "cover": examples[s][1], "ops": list(s[1])}
-                   for s in keep], f)
+        json.dump([{"n_leaves": examples[s][0], "cover": examples[s][1], "ops": list(s[1]),
+                    "owner_slot": examples[s][2], "world": examples[s][3]} for s in keep], f)
     print("%d distinct combine programs (%d kept) -> %s" % (len(shapes), len(keep), a.out))
 
 

@@ -34,6 +34,7 @@ def main():
     except Exception as exc:  # noqa: BLE001
         out["topo"] = repr(exc)
     if n >= 2 and all(attrs):
+        stage = "start"
         try:
             ctx = ok(cu.cuDevicePrimaryCtxRetain(ok(cu.cuDeviceGet(0))))
             ok(cu.cuCtxSetCurrent(ctx))
@@ -41,30 +42,42 @@ def main():
             prop.numDevices = n
             prop.handleTypes = cu.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR
             prop.size = 1 << 21
+            stage = "granularity"
+            gmin = ok(cu.cuMulticastGetGranularity(
+                prop, cu.CUmulticastGranularity_flags.CU_MULTICAST_GRANULARITY_MINIMUM))
             gran = ok(cu.cuMulticastGetGranularity(
                 prop, cu.CUmulticastGranularity_flags.CU_MULTICAST_GRANULARITY_RECOMMENDED))
-            size = max(gran, 1 << 21)
+            out["granularity"] = {"minimum": int(gmin), "recommended": int(gran)}
+            size = int(gran)
             prop.size = size
+            stage = "create"
             mc = ok(cu.cuMulticastCreate(prop))
             for d in range(n):
+                stage = "add_device %d" % d
                 ok(cu.cuMulticastAddDevice(mc, ok(cu.cuDeviceGet(d))))
             for d in range(n):
                 ap = cu.CUmemAllocationProp()
                 ap.type = cu.CUmemAllocationType.CU_MEM_ALLOCATION_TYPE_PINNED
                 ap.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
                 ap.location.id = d
+                ap.requestedHandleTypes = cu.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR
+                stage = "mem_create %d" % d
                 mem = ok(cu.cuMemCreate(size, ap, 0))
+                stage = "bind %d" % d
                 ok(cu.cuMulticastBindMem(mc, 0, mem, 0, size, 0))
-            va = ok(cu.cuMemAddressReserve(size, 0, 0, 0))
+            stage = "reserve"
+            va = ok(cu.cuMemAddressReserve(size, int(gran), 0, 0))
+            stage = "map"
             ok(cu.cuMemMap(va, size, 0, mc, 0))
             acc = cu.CUmemAccessDesc()
             acc.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
             acc.location.id = 0
             acc.flags = cu.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
+            stage = "set_access"
             ok(cu.cuMemSetAccess(va, size, [acc], 1))
-            out["multicast_object"] = {"ok": True, "granularity": int(gran), "size": int(size)}
+            out["multicast_object"] = {"ok": True, "size": int(size)}
         except Exception as exc:  # noqa: BLE001
-            out["multicast_object"] = {"ok": False, "error": repr(exc)[:300]}
+            out["multicast_object"] = {"ok": False, "stage": stage, "error": repr(exc)[:300]}
     print(json.dumps(out))
 
 

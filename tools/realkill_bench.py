@@ -66,16 +66,16 @@ def worker(rank, world, port, q, a):
         victims = set(range(VICTIM_RANK * per, (VICTIM_RANK + 1) * per))
         victim_range = {m for r in victims for m in range(r * G, (r + 1) * G)}
         step = {"t": -1}
+        bufs = {m: torch.empty_like(leaves[m]) for m in victim_range}
         regen = {}
 
         def leaf(m, rid):
             if step["t"] == a.fail_step and m in victim_range and rid not in victims:
                 if m not in regen:
-                    buf = torch.empty_like(leaves[m])
                     eng.mark("regen_a")
-                    make_leaf(m, out=buf)
+                    make_leaf(m, out=bufs[m])
                     eng.mark("regen_b")
-                    regen[m] = buf
+                    regen[m] = bufs[m]
                 return regen[m]
             return leaves[m]
 
@@ -100,6 +100,8 @@ def worker(rank, world, port, q, a):
                 rec = recovery_breakdown(eng)
                 eng.recovery_events = None
         mism = parity_check(eng, leaves, a.numel)
+        if getattr(inj, "shrinker", None) is not None:
+            inj.shrinker.join(timeout=60)
         det = inj.detections[0] if inj.detections else {}
         pre = step_ms[1:a.fail_step]  # step 0 warms up
         res = {
