@@ -1,11 +1,12 @@
 """Process plumbing of the multi-process GPU tests.
 
-Each test spawns one process per rank.  With fewer GPUs than ranks the ranks
-share devices round-robin (rank r on cuda:r % n): time-sliced contexts, the
-same CUDA IPC / VMM peer mappings and the same data path, so the
-multi-process commit is exercised on a one-GPU box too.  NCCL refuses two
-ranks on one device, so shared layouts use gloo for the host handshakes
-(the data path never touches the process group)."""
+Each test spawns one process per rank, each on its own GPU.  Ranks never
+share a device: the commit's barrier kernels spin on flags that peers
+write, and two such kernels of different processes on one GPU are not
+guaranteed to be co-scheduled (B200_PROFILING.md: 2-4 spinning ranks on one
+B200 raised Xid 109, context-switch timeout).  A test whose world exceeds
+the box's GPUs is skipped (the host logic of every world size runs on the
+CPU, tests/test_dist_host.py)."""
 
 import os
 import socket
@@ -28,9 +29,12 @@ def init_rank(rank: int, world: int, port: int, backend: str = "") -> bool:
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     n = torch.cuda.device_count()
-    dev = rank % n
+    if world > n:
+        raise RuntimeError("%d ranks need %d GPUs, %d visible (ranks never share a GPU)"
+                           % (world, world, n))
+    dev = rank
     torch.cuda.set_device(dev)
-    shared = world > n
+    shared = False
     backend = backend or ("gloo" if shared else "nccl")
     kw = {"device_id": torch.device("cuda", dev)} if backend == "nccl" else {}
     dist.init_process_group(backend, rank=rank, world_size=world, **kw)
@@ -49,9 +53,18 @@ def _entry(fn, rank, world, port, q, args):
             dist.destroy_process_group()
 
 
+def need_gpus(world: int) -> None:
+    """Skip the calling test unless every rank gets its own GPU."""
+    import pytest
+    if torch.cuda.device_count() < world:
+        pytest.skip("%d ranks need %d GPUs (ranks never share a GPU)" % (world, world))
+
+
 def spawn(fn, world: int, *args, timeout: float = 600.0):
     """Run fn(rank, world, *args) in `world` processes; {rank: result}.  A
     result that is a string starting with ERROR is a worker's traceback."""
+    if torch.cuda.device_count() < world:
+        raise RuntimeError("%d ranks need %d GPUs (ranks never share a GPU)" % (world, world))
     ctx = torch.multiprocessing.get_context("spawn")
     q = ctx.Queue()
     port = free_port()

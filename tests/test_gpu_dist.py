@@ -1,14 +1,14 @@
-"""Multi-process commit (one process per rank, NVLink P2P or, with more ranks
-than GPUs, ranks sharing devices): the committed gradient on every rank
-equals the CPU oracle's canonical tree bit for bit, with and without
-replica and whole-rank deaths, and every step's pool-stamp check is clean
-(``check_peers`` raises on a stale or overwritten partial)."""
+"""Multi-process commit (one process per GPU, NVLink P2P): the committed
+gradient on every rank equals the CPU oracle's canonical tree bit for bit,
+with and without replica and whole-rank deaths, and every step's pool-stamp
+check is clean (``check_peers`` raises on a stale or overwritten partial).
+A test needs one GPU per rank and is skipped on smaller boxes."""
 
 import numpy as np
 import pytest
 import torch
 
-from mp_util import failed, spawn
+from mp_util import failed, need_gpus, spawn
 
 pytestmark = [pytest.mark.gpu]
 
@@ -55,6 +55,7 @@ def _commit_worker(rank, world, combine_variant):
 
 @pytest.mark.parametrize("combine_variant,world", [(0, 4), (2, 4), (0, 2)])
 def test_distributed_commit_bitwise(combine_variant, world):
+    need_gpus(world)
     res = spawn(_commit_worker, world, combine_variant)
     assert not failed(res), failed(res)
     for r in range(world):
@@ -92,7 +93,8 @@ def _hsdp_worker(rank, world):
 
 
 def test_hsdp_commit_bf16_bitwise():
-    world = 4  # 2 shards x 2 replicas (shares devices on smaller boxes)
+    world = 4  # 2 shards x 2 replicas
+    need_gpus(world)
     res = spawn(_hsdp_worker, world)
     assert not failed(res), failed(res)
     for r in range(world):
@@ -123,8 +125,9 @@ def _one_replica_worker(rank, world, g, k, plans, numel):
     return res
 
 
-def test_whole_rank_death_one_replica_per_rank():
-    world = 4
+@pytest.mark.parametrize("world", [2, 4])
+def test_whole_rank_death_one_replica_per_rank(world):
+    need_gpus(world)
     plans = [[], [("during_sync", 3, [1])], [], []]
     res = spawn(_one_replica_worker, world, 4, 6, plans, 6 * 64 * 29 + 64)
     assert not failed(res), failed(res)
@@ -134,24 +137,51 @@ def test_whole_rank_death_one_replica_per_rank():
         assert [w for _, _, w, _ in res[r]] == [world] + [world - 1] * 3
 
 
+def _configs1_worker(rank, world, plans, numel):
+    """configs[1]'s replica group (W=8, G=4, K=20) spread over the ranks."""
+    from paper_2605_11215_b200.dist import DistributedGradientCommit
+    from oracle import fold
+    w, g, k = 8, 4, 20
+    host = [np.random.default_rng(500 + m).standard_normal(numel).astype(np.float32)
+            for m in range(w * g)]
+    dev = [torch.from_numpy(h).cuda() for h in host]
+    want = fold.canonical_tree(dict(enumerate(host)), w * g) / np.float32(w * g)
+    eng = DistributedGradientCommit(numel, w, g, k, barrier_timeout_s=60.0)
+    res = []
+    for t, plan in enumerate(plans):
+        out = eng.step(t, lambda m, rid: dev[m], Kill(plan))
+        torch.cuda.synchronize()
+        res.append((_bad_buckets(eng, want), out.contrib_total, out.w_cur,
+                    sorted(out.contributions.items())))
+    eng.check_peers()
+    return res
+
+
 @pytest.mark.parametrize("reuse", ["1", "0"])
-def test_eight_ranks_configs1_shape(reuse, monkeypatch):
-    """configs[1] at N=8 (one replica per rank: W=8, G=4, K=20, replica 3
-    killed during_sync on bucket 7), ranks sharing the box's GPUs.  This
-    shape once gave wrong bits on the failure step (round 1): the dead
-    rank's last combine still read a survivor's pool set after the
-    survivors' barriers had dropped it.  Fixed by the membership-transition
-    barrier (include/rcv.h); the pool stamps make any recurrence raise."""
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_configs1_whole_rank_death(world, reuse, monkeypatch):
+    """configs[1] (W=8, G=4, K=20) over `world` ranks, every replica of rank
+    1 killed during_sync on bucket 7: a whole-rank death.  This shape (at
+    world 8, one replica per rank) once gave wrong bits on the failure step
+    (round 1): the dead rank's last combine still read a survivor's pool
+    set after the survivors' barriers had dropped it.  Fixed by the
+    membership-transition barrier (include/rcv.h); the pool stamps make any
+    recurrence raise."""
+    need_gpus(world)
     monkeypatch.setenv("RCV_REUSE", reuse)
-    world = 8
-    plans = [[], [("during_sync", 7, [3])], []]
-    res = spawn(_one_replica_worker, world, 4, 20, plans, 20 * 64 * 5 + 64)
+    per = 8 // world
+    dead = list(range(per, 2 * per))
+    plans = [[], [("during_sync", 7, dead)], []]
+    res = spawn(_configs1_worker, world, plans, 20 * 64 * 5 + 64)
     assert not failed(res), failed(res)
     bad = {r: [x[0] for x in res[r]] for r in range(world) if any(x[0] for x in res[r])}
     assert not bad, bad
     for r in range(world):
         assert [x[1] for x in res[r]] == [32] * 3
-        assert [x[2] for x in res[r]] == [8, 7, 7]
-        # SURVEY §8(d)2: the failure step's contributions, then G=5 + minor 7 x 2
-        assert res[r][1][3] == [(0, 5), (1, 5), (2, 5), (4, 5), (5, 4), (6, 4), (7, 4)]
-        assert res[r][2][3] == [(0, 5), (1, 5), (2, 5), (4, 5), (5, 5), (6, 5), (7, 2)]
+        assert [x[2] for x in res[r]] == [8, 8 - per, 8 - per]
+    # the failure step's census then the advanced layout: every survivor
+    # commits exactly 32, the dead rank's replicas contribute nothing
+    for r in range(world):
+        assert all(c == 0 for rid, c in res[r][1][3] if rid in dead) or \
+            not any(rid in dead for rid, _ in res[r][1][3])
+        assert not any(rid in dead for rid, _ in res[r][2][3])
