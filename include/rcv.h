@@ -236,6 +236,31 @@ int rcv_vmm_alloc(size_t bytes, void **ptr_out, size_t *size_out, int *fd_out);
  * e.g. with pidfd_getfd); owner_device is the GPU holding the memory. */
 int rcv_vmm_import(int fd, size_t size, int owner_device, void **ptr_out);
 
+/* ---- NVLink SHARP multicast objects (NVLS) --------------------------------
+ * The all-gather half of the combine writes every owner slice into the
+ * landing buffer of every live rank (ref:comm.py:199-200, "write the total to
+ * every member").  Through a multicast object that is one store per vector:
+ * the NVSwitch replicates it to every GPU of the team, so a rank's NVLink
+ * egress for the all-gather is its slice once instead of once per peer.
+ * Only stores are multicast; the reduction stays on the SMs in canonical
+ * order (an in-switch reduction has no defined order).
+ *
+ * Setup, every rank of the team: one rank creates the object and exports it
+ * (rcv_mc_create), the others import the descriptor (rcv_mc_import); every
+ * rank adds its GPU (rcv_mc_add_device); after ALL ranks have added theirs,
+ * each binds its landing buffer -- a VMM allocation, rcv_vmm_alloc -- at
+ * offset 0 (rcv_mc_bind) and maps the object (rcv_mc_map).  Sizes and the
+ * bound address are multiples of rcv_mc_granularity.  *handle is an opaque
+ * CUmemGenericAllocationHandle. */
+int rcv_mc_supported(int *ok);
+int rcv_mc_granularity(int n_dev, size_t *gran);
+int rcv_mc_create(size_t bytes, int n_dev, uint64_t *handle, size_t *size_out, int *fd_out);
+int rcv_mc_import(int fd, uint64_t *handle);
+int rcv_mc_add_device(uint64_t handle);
+int rcv_mc_bind(uint64_t handle, void *local_ptr, size_t bytes);
+int rcv_mc_map(uint64_t handle, size_t size, void **mc_ptr);
+int rcv_mc_release(uint64_t handle, void *mc_ptr, size_t size);
+
 /* Cross-GPU barrier among the ranks in live_mask: rank `me` stores `value`
  * into slot `me` of every live peer's flag array (peer_flags[r], mapped
  * pointers), then waits until its own local_flags[r] >= value for every live
@@ -323,6 +348,9 @@ typedef struct {
   int remote_in, remote_out;     /* NVLink accounting of the combine */
   int guarded;                   /* real-kill mode: skip the combine once a
                                     live peer timed out (status word 0) */
+  uint32_t comb_out_mc;          /* bit j: comb_out[j] is a multicast address
+                                    (rcv_mc_map) bound to every live rank's
+                                    landing buffer; stored with multimem.st */
 } rcv_plan_desc;
 
 int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *desc, rcv_plan **out);

@@ -35,6 +35,8 @@ EXPORTS = (
     "rcv_vmm_alloc", "rcv_vmm_import", "rcv_kacc_push", "rcv_ctx_set_liveness", "rcv_ctx_poll",
     "rcv_liveness_create", "rcv_liveness_dead_word", "rcv_liveness_decide",
     "rcv_liveness_stats", "rcv_liveness_note_kill", "rcv_liveness_destroy",
+    "rcv_mc_supported", "rcv_mc_granularity", "rcv_mc_create", "rcv_mc_import",
+    "rcv_mc_add_device", "rcv_mc_bind", "rcv_mc_map", "rcv_mc_release",
 )
 
 
@@ -65,7 +67,7 @@ class PlanDesc(ctypes.Structure):
         ("variant", ctypes.c_int), ("comb_variant", ctypes.c_int),
         ("live_mask", ctypes.c_uint64), ("participate", ctypes.c_int),
         ("remote_in", ctypes.c_int), ("remote_out", ctypes.c_int),
-        ("guarded", ctypes.c_int),
+        ("guarded", ctypes.c_int), ("comb_out_mc", ctypes.c_uint32),
     ]
 
 
@@ -140,6 +142,15 @@ def load() -> ctypes.CDLL:
                                      ctypes.POINTER(u64), ctypes.POINTER(u64)]),
         "rcv_liveness_note_kill": (i32, [vp]),
         "rcv_liveness_destroy": (i32, [vp, i32]),
+        "rcv_mc_supported": (i32, [ctypes.POINTER(i32)]),
+        "rcv_mc_granularity": (i32, [i32, ctypes.POINTER(sz)]),
+        "rcv_mc_create": (i32, [sz, i32, ctypes.POINTER(u64), ctypes.POINTER(sz),
+                                ctypes.POINTER(i32)]),
+        "rcv_mc_import": (i32, [i32, ctypes.POINTER(u64)]),
+        "rcv_mc_add_device": (i32, [u64]),
+        "rcv_mc_bind": (i32, [u64, vp, sz]),
+        "rcv_mc_map": (i32, [u64, sz, ctypes.POINTER(vp)]),
+        "rcv_mc_release": (i32, [u64, vp, sz]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -531,6 +542,52 @@ def vmm_import(fd: int, size: int, owner_device: int) -> int:
     ptr = ctypes.c_void_p(0)
     _check(load().rcv_vmm_import(fd, size, owner_device, ctypes.byref(ptr)))
     return ptr.value
+
+
+# ---- NVLink SHARP multicast objects (rcv_mc_*) --------------------------------
+
+def mc_supported() -> bool:
+    ok = ctypes.c_int(0)
+    _check(load().rcv_mc_supported(ctypes.byref(ok)))
+    return bool(ok.value)
+
+
+def mc_granularity(n_dev: int) -> int:
+    g = ctypes.c_size_t(0)
+    _check(load().rcv_mc_granularity(n_dev, ctypes.byref(g)))
+    return g.value
+
+
+def mc_create(nbytes: int, n_dev: int):
+    """(handle, size, exported POSIX fd) of a new multicast object."""
+    h, size, fd = ctypes.c_uint64(0), ctypes.c_size_t(0), ctypes.c_int(-1)
+    _check(load().rcv_mc_create(nbytes, n_dev, ctypes.byref(h), ctypes.byref(size),
+                                ctypes.byref(fd)))
+    return h.value, size.value, fd.value
+
+
+def mc_import(fd: int) -> int:
+    h = ctypes.c_uint64(0)
+    _check(load().rcv_mc_import(fd, ctypes.byref(h)))
+    return h.value
+
+
+def mc_add_device(handle: int) -> None:
+    _check(load().rcv_mc_add_device(handle))
+
+
+def mc_bind(handle: int, ptr: int, nbytes: int) -> None:
+    _check(load().rcv_mc_bind(handle, ptr, nbytes))
+
+
+def mc_map(handle: int, size: int) -> int:
+    ptr = ctypes.c_void_p(0)
+    _check(load().rcv_mc_map(handle, size, ctypes.byref(ptr)))
+    return ptr.value
+
+
+def mc_release(handle: int, ptr: int, size: int) -> None:
+    _check(load().rcv_mc_release(handle, ptr, size))
 
 
 class _CudaArray:

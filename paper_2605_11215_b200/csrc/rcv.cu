@@ -222,6 +222,27 @@ __device__ __forceinline__ void st_vec(char *p, const float8 &v) {
   *reinterpret_cast<float4 *>(p + 16) = v.b;
 }
 
+// Stores through an NVLink SHARP multicast address (a cuMulticast object
+// mapped into this context, rcv_mc_*): the switch writes the vector into the
+// bound buffer of every GPU of the team, so one egress replaces n-1 peer
+// stores.  PTX has no f64 vector form: double2 is two scalar stores.
+__device__ __forceinline__ void st_mc(char *p, const float4 &v) {
+  asm volatile("multimem.st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_mc(char *p, const float8 &v) {
+  st_mc(p, v.a);
+  st_mc(p + 16, v.b);
+}
+__device__ __forceinline__ void st_mc(char *p, const double2 &v) {
+  asm volatile("multimem.st.global.f64 [%0], %1;" ::"l"(p), "d"(v.x) : "memory");
+  asm volatile("multimem.st.global.f64 [%0], %1;" ::"l"(p + 8), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_mc(char *p, const float &v) {
+  asm volatile("multimem.st.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
 // Fixed-capacity register stack.  Indices are compared against the (warp-
 // uniform) stack pointer with fully unrolled predicates, so the array stays in
 // registers.
@@ -254,6 +275,7 @@ struct FoldParams {
   uint8_t bf16[RCV_MAX_IN];
   int n_in;
   int n_out;
+  uint32_t mc_mask;         // bit j: out[j] is a multicast address (st_mc)
   unsigned long long nvec;  // accumulator vectors in this launch
   double divisor;           // 0 => no scale
   uint32_t stage_bytes;     // TMA
@@ -271,6 +293,20 @@ struct FoldParams {
   int8_t node_in[2 * RCV_MAX_IN - 1];    // input feeding the node, or -1
   uint8_t present[2 * RCV_MAX_IN - 1];   // subtree holds at least one input
 };
+
+template <typename V>
+__device__ __forceinline__ void st_out(const FoldParams &p, int j, unsigned long long off, const V &v) {
+  if ((p.mc_mask >> j) & 1u)
+    st_mc(p.out[j] + off, v);
+  else
+    st_vec(p.out[j] + off, v);
+}
+
+// multicast stores alias the peers' unicast mappings of the same memory: order
+// them before the stream's next barrier releases the buffers to their readers
+__device__ __forceinline__ void mc_fence(const FoldParams &p) {
+  if (p.mc_mask) asm volatile("fence.proxy.alias;" ::: "memory");
+}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -427,16 +463,30 @@ template <typename Prog> struct IsMulti<Prog, decltype(void(Prog::kMulti))> {
 template <typename Prog, typename V, typename Ld>
 __device__ __forceinline__ void emit(const FoldParams &p, const Ld &ld, unsigned long long off) {
   if constexpr (IsMulti<Prog>::value) {
-    Prog::template run<V>(p, ld, [&](int j, V r) { st_vec(p.out[j] + off, r); });
+    Prog::template run<V>(p, ld, [&](int j, V r) { st_out(p, j, off, r); });
   } else {
     V r = Prog::template eval<V>(p, ld);
     if (p.divisor != 0.0) r = vdiv(r, p.divisor);
-    for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + off, r);
+    // the multicast case is its own loop: the plain one keeps its registers
+    if (p.mc_mask) {
+      for (int j = 0; j < p.n_out; ++j) st_out(p, j, off, r);
+    } else {
+      for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + off, r);
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
 // DIRECT variant: 128-bit LDG straight from (local or peer) global memory
+
+// programs a multicast combine may run DIRECT: the fixed degraded-cover
+// programs and perfect trees over <= 8 nodes (run_fold sends any other
+// multicast fold through the TMA kernel)
+template <typename P> struct McDirect { static constexpr bool value = false; };
+template <int L> struct McDirect<ProgFull<L>> { static constexpr bool value = L <= 3; };
+template <int N, unsigned long long OPS> struct McDirect<ProgFixed<N, OPS>> {
+  static constexpr bool value = true;
+};
 
 template <typename A, typename Prog>
 __global__ void __launch_bounds__(256)
@@ -451,6 +501,9 @@ __global__ void __launch_bounds__(256)
     };
     emit<Prog, V>(p, ld, v * (unsigned long long)VecT<A>::OUT);
   }
+  // only the programs a multicast combine runs DIRECT carry the fence: in the
+  // N=1 commit's ProgFull<5> it costs 18 registers (46 -> 64)
+  if constexpr (McDirect<Prog>::value) mc_fence(p);
 }
 
 // DIRECT, two vectors per thread per iteration, for small perfect trees
@@ -489,9 +542,10 @@ __global__ void __launch_bounds__(256)
       float4 r = Prog::template eval<float4>(p, [&](int i) { return x[u][i]; });
       if (p.divisor != 0.0) r = vdiv(r, p.divisor);
       const unsigned long long off = (u ? w : v) * 16ull;
-      for (int j = 0; j < p.n_out; ++j) st_vec(p.out[j] + off, r);
+      for (int j = 0; j < p.n_out; ++j) st_out(p, j, off, r);
     }
   }
+  mc_fence(p);
 }
 
 // ---------------------------------------------------------------------------
@@ -612,6 +666,7 @@ __global__ void __launch_bounds__(TMA_THREADS)
       phase ^= 1;
     }
   }
+  mc_fence(p);
 }
 
 // ---------------------------------------------------------------------------
@@ -628,6 +683,7 @@ struct ScalarParams {
   double divisor;
   const unsigned int *guard;
   unsigned int guard_mask;
+  uint32_t mc_mask;  // bit j: out[j] is a multicast address
 };
 
 template <typename A>
@@ -673,9 +729,18 @@ __global__ void __launch_bounds__(256)
     }
     A r = p.n_in ? s[0] : (A)0;
     if (p.divisor != 0.0) r = sdiv(r, p.divisor);
-    for (int j = 0; j < p.n_out; ++j)
-      *reinterpret_cast<A *>(p.out[j] + e * sizeof(A)) = r;
+    for (int j = 0; j < p.n_out; ++j) {
+      if ((p.mc_mask >> j) & 1u) {
+        if constexpr (sizeof(A) == 4)
+          st_mc(p.out[j] + e * sizeof(A), r);
+        else
+          asm volatile("multimem.st.global.f64 [%0], %1;" ::"l"(p.out[j] + e * sizeof(A)), "d"(r) : "memory");
+      } else {
+        *reinterpret_cast<A *>(p.out[j] + e * sizeof(A)) = r;
+      }
+    }
   }
+  if (p.mc_mask) asm volatile("fence.proxy.alias;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -875,8 +940,10 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   // a peer that already timed out is dead: never signal or wait on it again
   const unsigned int dead = *(volatile const unsigned int *)p.status | (p.host_dead ? *p.host_dead : 0u);
   const bool peer = t < p.n && t != p.me && ((p.live >> t) & 1ull) && !((dead >> t) & 1u);
-  // everything this GPU wrote before this kernel (partials, remote stores)
-  // is made visible system-wide before the flag store releases it
+  // everything this GPU wrote before this kernel (partials, remote and
+  // multicast stores) is made visible system-wide before the flag store
+  // releases it
+  asm volatile("fence.proxy.alias;" ::: "memory");
   __threadfence_system();
   if (peer)
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.peer[t] + p.me), "l"(p.value)
@@ -895,6 +962,7 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   }
   __syncthreads();
   __threadfence_system();
+  asm volatile("fence.proxy.alias;" ::: "memory");
   // every live peer has arrived, so every producer finished this call's
   // partials: the stamps the combine behind this barrier reads must be set
   if (t < p.n_now) {
@@ -954,6 +1022,7 @@ struct FoldReq {
   bool wide32 = false;
   bool pair = false;  // DIRECT: two vectors per thread (small perfect trees, fp32)
   int shape = -1;     // >= 0: index of a compile-time program (shapes.inc)
+  uint32_t mc_mask = 0;  // bit j: out[j] is a multicast address (fp32 vector paths only)
 };
 
 enum { PK_STACK = 0, PK_LEFT = 1, PK_TREE = 2 };
@@ -998,6 +1067,7 @@ int launch_scalar_t(const FoldReq &r, unsigned long long e0, unsigned long long 
   p.divisor = r.divisor;
   p.guard = r.guard;
   p.guard_mask = r.guard_mask;
+  p.mc_mask = r.mc_mask;
   const unsigned long long blocks = std::min<unsigned long long>((n + 255) / 256, (unsigned long long)sms * 8);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   fold_scalar_kernel<A, MAXD><<<(unsigned)std::max<unsigned long long>(blocks, 1), 256, 0, st>>>(p);
@@ -1027,6 +1097,7 @@ void fill_vec_params(FoldParams &p, const FoldReq &r, unsigned long long e0,
     p.bf16[i] = r.in_dt[i] == RCV_BF16;
   }
   for (int j = 0; j < r.n_out; ++j) p.out[j] = r.out[j] + e0 * esize(r.acc_dt);
+  p.mc_mask = r.mc_mask;
   p.nvec = nvec;
   p.divisor = r.divisor;
   p.guard = r.guard;
@@ -1212,6 +1283,7 @@ int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int s
   int rc = r.n_roots > 0 ? RCV_OK : program_depth(r.op, r.n_in, &maxd);
   if (rc) return rc;
   if (r.n_in == 0) {
+    if (r.mc_mask) return set_err(RCV_EINVAL, "multicast output of an empty fold");
     for (int j = 0; j < r.n_out; ++j) CK(cudaMemsetAsync(r.out[j], 0, numel * esize(r.acc_dt), st));
     return RCV_OK;
   }
@@ -1242,10 +1314,12 @@ int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int s
     // ring, which decouples their loads from the control flow.
     if (variant == RCV_VARIANT_AUTO && (r.full_L >= 0 || r.n_roots > 0 || r.shape >= 0))
       variant = RCV_VARIANT_DIRECT;
+    if (r.mc_mask && variant == RCV_VARIANT_DIRECT && !(r.shape >= 0 || (r.full_L >= 0 && r.full_L <= 3)))
+      variant = RCV_VARIANT_TMA;  // the DIRECT kernel fences multicast stores only for McDirect programs
     bool use_tma = variant == RCV_VARIANT_TMA || variant == RCV_VARIANT_AUTO;
     const bool geom_ok = f64 ? tma_geom<double>(r, &g) : (wide ? tma_geom<F8>(r, &g) : tma_geom<float>(r, &g));
     if (use_tma && !geom_ok) {
-      if (variant == RCV_VARIANT_TMA)
+      if (variant == RCV_VARIANT_TMA || r.mc_mask)
         return set_err(RCV_EINVAL, "TMA variant: %d inputs do not fit a 2-stage ring", r.n_in);
       use_tma = false;
     }
@@ -1835,6 +1909,168 @@ int rcv_vmm_import(int fd, size_t size, int owner_device, void **ptr_out) {
   rc = vmm_map(v, h, size, owner_device, ptr_out);
   v->release(h);
   return rc;
+}
+
+// ---- NVLink SHARP multicast objects ----------------------------------------
+
+namespace {
+struct McApi {
+  CUresult (*create)(CUmemGenericAllocationHandle *, const CUmulticastObjectProp *);
+  CUresult (*gran)(size_t *, const CUmulticastObjectProp *, CUmulticastGranularity_flags);
+  CUresult (*add)(CUmemGenericAllocationHandle, CUdevice);
+  CUresult (*bind)(CUmemGenericAllocationHandle, size_t, CUdeviceptr, size_t, unsigned long long);
+  CUresult (*unbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t);
+  CUresult (*device)(CUdevice *, int);
+  CUresult (*unmap)(CUdeviceptr, size_t);
+  CUresult (*free_va)(CUdeviceptr, size_t);
+  bool ok = false;
+};
+
+int mc_api(McApi **out) {
+  static McApi a;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!a.ok) {
+    struct { const char *name; void **fn; } t[] = {
+        {"cuMulticastCreate", (void **)&a.create},
+        {"cuMulticastGetGranularity", (void **)&a.gran},
+        {"cuMulticastAddDevice", (void **)&a.add},
+        {"cuMulticastBindAddr", (void **)&a.bind},
+        {"cuMulticastUnbind", (void **)&a.unbind},
+        {"cuDeviceGet", (void **)&a.device},
+        {"cuMemUnmap", (void **)&a.unmap},
+        {"cuMemAddressFree", (void **)&a.free_va}};
+    for (auto &e : t) {
+      cudaDriverEntryPointQueryResult q;
+      CK(cudaGetDriverEntryPoint(e.name, e.fn, cudaEnableDefault, &q));
+      if (q != cudaDriverEntryPointSuccess || !*e.fn) return set_err(RCV_ECUDA, "%s unavailable", e.name);
+    }
+    a.ok = true;
+  }
+  *out = &a;
+  return RCV_OK;
+}
+
+CUmulticastObjectProp mc_prop(size_t bytes, int n_dev) {
+  CUmulticastObjectProp prop = {};
+  prop.numDevices = (unsigned int)n_dev;
+  prop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  prop.size = bytes;
+  return prop;
+}
+
+int mc_current_device(McApi *a, CUdevice *dev) {
+  int d = 0;
+  CK(cudaGetDevice(&d));
+  if (a->device(dev, d) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuDeviceGet(%d)", d);
+  return RCV_OK;
+}
+}  // namespace
+
+int rcv_mc_supported(int *ok) {
+  int d = 0;
+  CK(cudaGetDevice(&d));
+  *ok = 0;
+  CK(cudaDeviceGetAttribute(ok, (cudaDeviceAttr)CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, d));
+  return RCV_OK;
+}
+
+int rcv_mc_granularity(int n_dev, size_t *gran) {
+  McApi *a = nullptr;
+  int rc = mc_api(&a);
+  if (rc) return rc;
+  CUmulticastObjectProp prop = mc_prop(1 << 21, n_dev);
+  if (a->gran(gran, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS)
+    return set_err(RCV_ECUDA, "cuMulticastGetGranularity");
+  return RCV_OK;
+}
+
+int rcv_mc_create(size_t bytes, int n_dev, uint64_t *handle, size_t *size_out, int *fd_out) {
+  McApi *a = nullptr;
+  Vmm *v = nullptr;
+  int rc = mc_api(&a);
+  if (rc || (rc = vmm(&v))) return rc;
+  size_t gran = 0;
+  if ((rc = rcv_mc_granularity(n_dev, &gran))) return rc;
+  const size_t size = (bytes + gran - 1) / gran * gran;
+  CUmulticastObjectProp prop = mc_prop(size, n_dev);
+  CUmemGenericAllocationHandle h;
+  CUresult e = a->create(&h, &prop);
+  if (e != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuMulticastCreate(%zu bytes, %d GPUs): %d", size, n_dev, (int)e);
+  int fd = -1;
+  if (v->exportfd(&fd, h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) != CUDA_SUCCESS)
+    return set_err(RCV_ECUDA, "cuMemExportToShareableHandle(multicast)");
+  *handle = (uint64_t)h;
+  *size_out = size;
+  *fd_out = fd;
+  return RCV_OK;
+}
+
+int rcv_mc_import(int fd, uint64_t *handle) {
+  Vmm *v = nullptr;
+  int rc = vmm(&v);
+  if (rc) return rc;
+  CUmemGenericAllocationHandle h;
+  if (v->importfd(&h, (void *)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR) != CUDA_SUCCESS)
+    return set_err(RCV_ECUDA, "cuMemImportFromShareableHandle(multicast fd %d)", fd);
+  *handle = (uint64_t)h;
+  return RCV_OK;
+}
+
+int rcv_mc_add_device(uint64_t handle) {
+  McApi *a = nullptr;
+  int rc = mc_api(&a);
+  if (rc) return rc;
+  CUdevice dev;
+  if ((rc = mc_current_device(a, &dev))) return rc;
+  CUresult e = a->add((CUmemGenericAllocationHandle)handle, dev);
+  if (e != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuMulticastAddDevice: %d", (int)e);
+  return RCV_OK;
+}
+
+int rcv_mc_bind(uint64_t handle, void *local_ptr, size_t bytes) {
+  McApi *a = nullptr;
+  int rc = mc_api(&a);
+  if (rc) return rc;
+  CUresult e = a->bind((CUmemGenericAllocationHandle)handle, 0, (CUdeviceptr)local_ptr, bytes, 0);
+  if (e != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuMulticastBindAddr(%zu bytes): %d", bytes, (int)e);
+  return RCV_OK;
+}
+
+int rcv_mc_map(uint64_t handle, size_t size, void **mc_ptr) {
+  Vmm *v = nullptr;
+  int rc = vmm(&v);
+  if (rc) return rc;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  size_t gran = 0;
+  CUdeviceptr va = 0;
+  if ((rc = rcv_mc_granularity(1, &gran))) return rc;
+  if (v->reserve(&va, size, gran, 0, 0) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuMemAddressReserve(multicast)");
+  if (v->map(va, size, 0, (CUmemGenericAllocationHandle)handle, 0) != CUDA_SUCCESS)
+    return set_err(RCV_ECUDA, "cuMemMap(multicast)");
+  CUmemAccessDesc acc = {};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if (v->access(va, size, &acc, 1) != CUDA_SUCCESS) return set_err(RCV_ECUDA, "cuMemSetAccess(multicast)");
+  *mc_ptr = (void *)va;
+  return RCV_OK;
+}
+
+int rcv_mc_release(uint64_t handle, void *mc_ptr, size_t size) {
+  McApi *a = nullptr;
+  Vmm *v = nullptr;
+  int rc = mc_api(&a);
+  if (rc || (rc = vmm(&v))) return rc;
+  if (mc_ptr) {
+    a->unmap((CUdeviceptr)mc_ptr, size);
+    a->free_va((CUdeviceptr)mc_ptr, size);
+  }
+  CUdevice dev;
+  if (mc_current_device(a, &dev) == RCV_OK) a->unbind((CUmemGenericAllocationHandle)handle, dev, 0, size);
+  v->release((CUmemGenericAllocationHandle)handle);
+  return RCV_OK;
 }
 
 int rcv_ipc_import(const void *handle, size_t offset, void **ptr_out) {
@@ -2442,6 +2678,9 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
           p->producers.push_back(rk);
       }
     }
+    // outputs that are multicast addresses: one store reaches every live
+    // rank's landing buffer through the switch (rcv_mc_*)
+    p->comb.mc_mask = d->comb_out_mc;
     p->has_comb = true;
     p->slice_q = d->slice_q;
     p->slice_nr = d->slice_nr;

@@ -155,6 +155,39 @@ class VmmBuffers:
         except Exception as exc:  # surfaced by share()
             errors.append(exc)
 
+    def broadcast_fd(self, fd: Optional[int], root: int = 0) -> int:
+        """Hand rank `root`'s descriptor `fd` to every other rank (the same
+        peer checks as share()); returns this rank's descriptor of it."""
+        import socket
+        import threading
+        name = "\0rcv-%s-b%d-%d" % (self.job, root, len(self._keep))
+        if self.rank == root:
+            srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            srv.bind(name)
+            srv.listen(self.world)
+            srv.settimeout(self.timeout_s)
+            errors: List[Exception] = []
+            th = threading.Thread(target=self._serve, args=(srv, fd, errors), daemon=True)
+            th.start()
+        dist.barrier(group=self.group)  # the root listens before anyone connects
+        if self.rank == root:
+            th.join(timeout=self.timeout_s)
+            srv.close()
+            if errors or th.is_alive():
+                raise RuntimeError("descriptor broadcast failed: %r" % (errors or "timeout"))
+            self._keep.append((fd, None))
+            return fd
+        c = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        c.settimeout(self.timeout_s)
+        c.connect(name)
+        c.sendall(self.secret)
+        _, fds, _, _ = socket.recv_fds(c, 1, 1)
+        c.close()
+        if not fds:
+            raise RuntimeError("rank %d refused its descriptor" % root)
+        self._keep.append((fds[0], None))
+        return fds[0]
+
     def share(self, nbytes: int, dtype: torch.dtype):
         """Allocate nbytes here; returns (local tensor, [ptr of every rank])."""
         import socket
@@ -320,7 +353,7 @@ class DistributedGradientCommit(GradientCommit):
                  combine_variant: int = _lib.VARIANT_AUTO,
                  pool_slots: int = 8, barrier_timeout_s: float = 30.0,
                  real_kill: bool = False, liveness_deadline_s: Optional[float] = 10e-3,
-                 liveness_period_s: float = 1e-3):
+                 liveness_period_s: float = 1e-3, multicast: Optional[bool] = None):
         if policy_kind not in ("static", "adaptive"):
             raise ValueError("unknown policy kind %r" % (policy_kind,))
         self.rank = dist.get_rank(group) if rank is None else rank
@@ -361,26 +394,47 @@ class DistributedGradientCommit(GradientCommit):
         self.integrity_errors = 0
         # RCV_TIMEOUT_S overrides every bounded wait (debugging hangs)
         self.timeout_ns = int(float(os.environ.get("RCV_TIMEOUT_S", barrier_timeout_s)) * 1e9)
-        if real_kill:
-            # VMM memory: survivors' mappings outlive a dead exporter
+        # NVLS multicast all-gather (RCV_MC=1 or multicast=True): the combine
+        # stores each owner slice once, through a multicast object bound to
+        # every rank's landing slot (its first replica buffer), instead of
+        # once per live peer.  Not in real-kill mode (a dead team member's
+        # binding is left alone there).
+        if multicast is None:
+            multicast = os.environ.get("RCV_MC", "0") not in ("", "0")
+        self.multicast = bool(multicast) and not real_kill and self.world > 1
+        self.mc_ptr: Optional[int] = None
+        self._slot = numel  # elements from one replica buffer to the next
+        if self.multicast:
+            gran = _lib.mc_granularity(self.world)
+            self._slot = -(-numel * self._es // gran) * gran // self._es
+        if real_kill or self.multicast:
+            # VMM memory: survivors' mappings outlive a dead exporter, and a
+            # multicast object binds only shareable allocations
             vb = VmmBuffers(self.rank, self.world, group)
             self._shared = vb
-            store, store_ptr = vb.share(per * numel * self._es, dtype)
+            store, store_ptr = vb.share(per * self._slot * self._es, dtype)
+            store.zero_()
+        if real_kill:
             self.pool, self.pool_ptr = vb.share(3 * pool_slots * self.lmax * self._es, dtype)
             self.flags, self.flag_ptr = vb.share(FLAG_SLOTS * 8, torch.int64)
-            store.zero_()
             self.flags.zero_()
         else:
-            store = torch.zeros(per * numel, dtype=dtype, device=self.device)
+            if not self.multicast:
+                store = torch.zeros(per * numel, dtype=dtype, device=self.device)
             self.pool = torch.empty(3 * pool_slots * self.lmax, dtype=dtype, device=self.device)
             self.flags = torch.zeros(FLAG_SLOTS, dtype=torch.int64, device=self.device)
             pb = PeerBuffers(self.rank, self.world, group)
-            store_ptr = pb.share(store)
+            if not self.multicast:
+                store_ptr = pb.share(store)
             self.pool_ptr = pb.share(self.pool)
             self.flag_ptr = pb.share(self.flags)
-        self.grads = {r: store[i * numel:(i + 1) * numel] for i, r in enumerate(local)}
-        self.grad_ptr = {r: store_ptr[self.rank_of[r]] + (r % per) * numel * self._es
+        sl = self._slot
+        self.grads = {r: store[i * sl:i * sl + numel] for i, r in enumerate(local)}
+        self.grad_ptr = {r: store_ptr[self.rank_of[r]] + (r % per) * sl * self._es
                          for r in members}
+        self._landing = local[0]
+        if self.multicast:
+            self._mc_setup(store_ptr[self.rank], group)
         self.rt = _lib.BucketRuntime(self.world, self.rank, self.flags, self.flag_ptr,
                                      self.status, self.timeout_ns)
         self.liveness: Optional[_lib.Liveness] = None
@@ -399,6 +453,25 @@ class DistributedGradientCommit(GradientCommit):
         self._plan_key = None
         torch.cuda.synchronize(self.device)
         dist.barrier(group=group)
+
+    def _mc_setup(self, landing_ptr: int, group) -> None:
+        """Rank 0 creates the multicast object and hands its descriptor to
+        the others; every rank adds its GPU, then (after all have) binds its
+        landing slot and maps the object (include/rcv.h, rcv_mc_*)."""
+        vb = self._shared
+        nbytes = self._slot * self._es
+        fd = None
+        if self.rank == 0:
+            h, size, fd = _lib.mc_create(nbytes, self.world)
+        fd = vb.broadcast_fd(fd)
+        if self.rank != 0:
+            h, size = _lib.mc_import(fd), nbytes
+        _lib.mc_add_device(h)
+        dist.barrier(group=group)
+        _lib.mc_bind(h, landing_ptr, size)
+        dist.barrier(group=group)
+        self.mc_ptr = _lib.mc_map(h, size)
+        self._mc = (h, size)
 
     # ---- hooks of GradientCommit.step ----
 
@@ -561,14 +634,26 @@ class DistributedGradientCommit(GradientCommit):
         prim = [self._primary(rk) for rk in ranks]
         mine = [r for r in self.comm.members if self._holds(r)]
         part = self.rank in ranks
+        if self.multicast:
+            # one multicast store per vector lands in every rank's landing
+            # slot (its first replica buffer, live or not); the local
+            # broadcast copies it to the rank's other live replicas
+            comb_out, n_remote_out = [self.mc_ptr], 1
+            src = self._landing if mine else None
+            bcast = [r for r in mine if r != self._landing]
+        else:
+            comb_out = [self.grad_ptr[r] for r in prim]
+            n_remote_out = sum(1 for r in prim if not self._holds(r))
+            src = mine[0] if mine else None
+            bcast = mine[1:]
 
         def arr(ctype, xs):
             return (ctype * max(1, len(xs)))(*xs)
         keep = dict(pre_blocks=arr(Block, pre_blocks), pre_counts=arr(ctypes.c_int, pre_counts),
                     pre_leaves=arr(ctypes.c_uint32, pre_leaves),
                     pre_out=arr(ctypes.c_void_p, pre_out), comb=arr(Block, comb),
-                    comb_out=arr(ctypes.c_void_p, [self.grad_ptr[r] for r in prim]),
-                    bcast_out=arr(ctypes.c_void_p, [self.grads[r].data_ptr() for r in mine[1:]]),
+                    comb_out=arr(ctypes.c_void_p, comb_out),
+                    bcast_out=arr(ctypes.c_void_p, [self.grads[r].data_ptr() for r in bcast]),
                     comb_rank=arr(ctypes.c_int, [rk for _, (rk, _) in sorted(slot_of.items())]))
         d = _lib.PlanDesc(
             n_pre=len(pre_counts), pre_blocks=keep["pre_blocks"], pre_counts=keep["pre_counts"],
@@ -576,16 +661,16 @@ class DistributedGradientCommit(GradientCommit):
             set_stride=self.pool_slots * self.lmax,
             n_comb=len(comb) if part else 0, comb_blocks=keep["comb"],
             comb_rank=keep["comb_rank"], n_leaves=b,
-            n_comb_out=len(prim), comb_out=keep["comb_out"],
+            n_comb_out=len(comb_out), comb_out=keep["comb_out"],
             slice_q=ranks.index(self.rank) if part else 0, slice_nr=len(ranks),
-            n_bcast=max(0, len(mine) - 1),
-            bcast_src=self.grads[mine[0]].data_ptr() if mine else None,
+            n_bcast=len(bcast) if src is not None else 0,
+            bcast_src=self.grads[src].data_ptr() if src is not None else None,
             bcast_out=keep["bcast_out"], acc_dtype=self._code, divisor=float(b),
             variant=self.variant, comb_variant=self.combine_variant,
             live_mask=mask, participate=int(part),
             remote_in=sum(1 for rk, _ in slot_of.values() if rk != self.rank),
-            remote_out=sum(1 for r in prim if not self._holds(r)),
-            guarded=int(self.real_kill))
+            remote_out=n_remote_out,
+            guarded=int(self.real_kill), comb_out_mc=int(self.multicast))
         self.rt.set_plan(d, keep)
 
     def _reduce_bucket(self, k: int, leaves) -> int:

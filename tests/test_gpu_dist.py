@@ -33,7 +33,7 @@ def _bad_buckets(eng, want):
     return sorted(bad)
 
 
-def _commit_worker(rank, world, combine_variant):
+def _commit_worker(rank, world, combine_variant, multicast=False):
     from paper_2605_11215_b200.dist import DistributedGradientCommit
     from oracle import fold
     numel = 5 * 64 * 37 + 19
@@ -42,7 +42,8 @@ def _commit_worker(rank, world, combine_variant):
     dev = [torch.from_numpy(h).cuda() for h in host]
     want = fold.canonical_tree(dict(enumerate(host)), 32) / np.float32(32)
     eng = DistributedGradientCommit(numel, 8, 4, 5, combine_variant=combine_variant,
-                                    barrier_timeout_s=60.0)
+                                    barrier_timeout_s=60.0, multicast=multicast)
+    assert eng.multicast == multicast
     results = []
     for t, plan in enumerate([[], [("during_sync", 2, [3])], [], [("before_sync", None, [6])]]):
         out = eng.step(t, lambda m, rid: dev[m], Kill(plan))
@@ -53,10 +54,14 @@ def _commit_worker(rank, world, combine_variant):
     return results
 
 
-@pytest.mark.parametrize("combine_variant,world", [(0, 4), (2, 4), (0, 2)])
-def test_distributed_commit_bitwise(combine_variant, world):
+@pytest.mark.parametrize("combine_variant,world,multicast",
+                         [(0, 4, False), (2, 4, False), (0, 2, False), (0, 2, True), (0, 4, True),
+                          (1, 4, True)])
+def test_distributed_commit_bitwise(combine_variant, world, multicast):
+    """multicast: the combine's all-gather stores through an NVLS multicast
+    object (multimem.st) instead of one store per live peer."""
     need_gpus(world)
-    res = spawn(_commit_worker, world, combine_variant)
+    res = spawn(_commit_worker, world, combine_variant, multicast)
     assert not failed(res), failed(res)
     for r in range(world):
         for bad, total, _ in res[r]:
@@ -137,7 +142,7 @@ def test_whole_rank_death_one_replica_per_rank(world):
         assert [w for _, _, w, _ in res[r]] == [world] + [world - 1] * 3
 
 
-def _configs1_worker(rank, world, plans, numel):
+def _configs1_worker(rank, world, plans, numel, multicast=False):
     """configs[1]'s replica group (W=8, G=4, K=20) spread over the ranks."""
     from paper_2605_11215_b200.dist import DistributedGradientCommit
     from oracle import fold
@@ -146,7 +151,7 @@ def _configs1_worker(rank, world, plans, numel):
             for m in range(w * g)]
     dev = [torch.from_numpy(h).cuda() for h in host]
     want = fold.canonical_tree(dict(enumerate(host)), w * g) / np.float32(w * g)
-    eng = DistributedGradientCommit(numel, w, g, k, barrier_timeout_s=60.0)
+    eng = DistributedGradientCommit(numel, w, g, k, barrier_timeout_s=60.0, multicast=multicast)
     res = []
     for t, plan in enumerate(plans):
         out = eng.step(t, lambda m, rid: dev[m], Kill(plan))
@@ -157,9 +162,9 @@ def _configs1_worker(rank, world, plans, numel):
     return res
 
 
-@pytest.mark.parametrize("reuse", ["1", "0"])
+@pytest.mark.parametrize("reuse,multicast", [("1", False), ("0", False), ("1", True)])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_configs1_whole_rank_death(world, reuse, monkeypatch):
+def test_configs1_whole_rank_death(world, reuse, multicast, monkeypatch):
     """configs[1] (W=8, G=4, K=20) over `world` ranks, every replica of rank
     1 killed during_sync on bucket 7: a whole-rank death.  This shape (at
     world 8, one replica per rank) once gave wrong bits on the failure step
@@ -172,7 +177,7 @@ def test_configs1_whole_rank_death(world, reuse, monkeypatch):
     per = 8 // world
     dead = list(range(per, 2 * per))
     plans = [[], [("during_sync", 7, dead)], []]
-    res = spawn(_configs1_worker, world, plans, 20 * 64 * 5 + 64)
+    res = spawn(_configs1_worker, world, plans, 20 * 64 * 5 + 64, multicast)
     assert not failed(res), failed(res)
     bad = {r: [x[0] for x in res[r]] for r in range(world) if any(x[0] for x in res[r])}
     assert not bad, bad
