@@ -430,13 +430,23 @@ def run_ours(args):
     with Clocks(local) as clk:
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
+        # every rank enters the timed region together (the clock sampler's
+        # start-up differs per rank, and the max over ranks would otherwise
+        # count one rank's wait for the slowest one's first barrier)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+            torch.cuda.synchronize()
         start.record(stream)
         t_host = time.perf_counter()
+        host_step = []
         for s in range(args.warmup, total_steps):
             kill.step = s
             a = torch.cuda.Event(enable_timing=True)
             a.record(stream)
+            h0 = time.perf_counter()
             outcomes.append(eng.step(s, leaf, kill))
+            host_step.append((time.perf_counter() - h0) * 1e3)
             step_ev.append(a)
         end.record(stream)
         host_ms = (time.perf_counter() - t_host) * 1e3 / args.steps
@@ -524,6 +534,12 @@ def run_ours(args):
                     "degraded_median": statistics.median(post) if post else None,
                     "all": [round(x, 3) for x in step_ms]},
         "host_enqueue_ms_per_step": host_ms,
+        # host time inside eng.step (control plane + launches): a step whose
+        # host time exceeds its device time leaves the GPU waiting
+        "host_step_ms": {"failure_free_median": statistics.median(host_step[:fail_idx[0]])
+                         if fail_idx and fail_idx[0] > 0 else statistics.median(host_step),
+                         "degraded_median": statistics.median(host_step[fail_idx[-1] + 1:])
+                         if fail_idx and fail_idx[-1] + 1 < len(host_step) else None},
         "gpu_launches": n_launch,
         "kernel_pass": "per-kernel rows from 3 failure-free steps timed launch by launch (CUDA events on each launch's stream) before the headline region",
         "clocks": clk.summary(),
