@@ -611,12 +611,9 @@ def roofline(dom, per_kind, peak, peak_kind, world=1):
         # rank, a perfect tree of world leaves, which AUTO runs DIRECT
         return {"bound": "nvlink", "achieved": ach, "peak": NVLINK_PEAK, "unit": "GB/s",
                 "frac": ach / NVLINK_PEAK, "traffic": None, "peak_kind": "measured peer copy",
-                "kernel": "%s<ProgFull<%d>> combine over peer pointers "
-                          "(failure-free cover; degraded covers run fold_tma_kernel<F8, ProgTree<L>>, "
-                          "see kernels_degraded)" % (
-                              "fold_direct_pair_kernel" if world <= 8 and
-                              os.environ.get("RCV_PAIR", "1") not in ("", "0")
-                              else "fold_direct_kernel<float>", max(0, world.bit_length() - 1)),
+                "kernel": "fold_direct_pair_kernel<ProgFull<%d>> combine over peer pointers "
+                          "(failure-free cover; degraded covers run the fixed programs of "
+                          "shapes.inc, see kernels_degraded)" % max(0, world.bit_length() - 1),
                 "mean_launch_us": k["mean_launch_us"], "launches_timed": k["launches"],
                 "hbm_gbs": k["hbm_gbs"]}
     return {"bound": "hbm", "achieved": k["hbm_gbs"], "peak": peak, "unit": "GB/s",
