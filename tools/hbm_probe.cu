@@ -201,10 +201,17 @@ __device__ __forceinline__ F8v ld8(const F8v *p) {
   }
   return v;
 }
+template <int SMODE = 0>
 __device__ __forceinline__ void st8(F8v *p, const F8v &v) {
-  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v.a.x), "f"(v.a.y),
-               "f"(v.a.z), "f"(v.a.w), "f"(v.b.x), "f"(v.b.y), "f"(v.b.z), "f"(v.b.w)
-               : "memory");
+  if constexpr (SMODE == 0) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v.a.x), "f"(v.a.y),
+                 "f"(v.a.z), "f"(v.a.w), "f"(v.b.x), "f"(v.b.y), "f"(v.b.z), "f"(v.b.w)
+                 : "memory");
+  } else {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v.a.x), "f"(v.a.y),
+                 "f"(v.a.z), "f"(v.a.w), "f"(v.b.x), "f"(v.b.y), "f"(v.b.z), "f"(v.b.w)
+                 : "memory");
+  }
 }
 __device__ __forceinline__ F8v add8(const F8v &x, const F8v &y) { return F8v{add4(x.a, y.a), add4(x.b, y.b)}; }
 
@@ -219,7 +226,7 @@ __device__ __forceinline__ F8v tree8(const P &p, unsigned long long v) {
   }
 }
 
-template <int MODE>
+template <int MODE, int SMODE = 0>
 __global__ void __launch_bounds__(256) k_tree8(const __grid_constant__ P p) {
   const unsigned long long n8 = p.nvec / 2;
   for (unsigned long long v = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; v < n8;
@@ -228,7 +235,7 @@ __global__ void __launch_bounds__(256) k_tree8(const __grid_constant__ P p) {
     r.a = div4(r.a, 32.f);
     r.b = div4(r.b, 32.f);
 #pragma unroll
-    for (int j = 0; j < NOUT; ++j) st8(reinterpret_cast<F8v *>(p.out[j]) + v, r);
+    for (int j = 0; j < NOUT; ++j) st8<SMODE>(reinterpret_cast<F8v *>(p.out[j]) + v, r);
   }
 }
 
@@ -280,6 +287,18 @@ int main() {
            name, grid, best, best * 1e3 / K, bytes / (best * 1e-3) / 1e9);
     fflush(stdout);
   };
+  const char *only = getenv("PROBE_ONLY");
+  if (only) {  // the follow-up: 256-bit loads with streaming stores, larger grids
+    const int grids2[] = {sms * 3, sms * 6, sms * 12, sms * 16, sms * 24, sms * 32};
+    for (int g : grids2) {
+      run("w256", 32, 8, g, [](int grid, const P &p) { k_tree8<1, 0><<<grid, 256>>>(p); });
+      run("w256cs", 32, 8, g, [](int grid, const P &p) { k_tree8<1, 1><<<grid, 256>>>(p); });
+      run("w256vcs", 32, 8, g, [](int grid, const P &p) { k_tree8<0, 1><<<grid, 256>>>(p); });
+      run("hint", 32, 8, g, [](int grid, const P &p) { k_tree<2><<<grid, 256>>>(p); });
+      run("read", 32, 0, g, [](int grid, const P &p) { k_read<<<grid, 256>>>(p); });
+    }
+    return 0;
+  }
   const int grids[] = {sms * 2, sms * 4, sms * 5, sms * 8, sms * 16};
   for (int g : grids) {
     run("base", 32, 8, g, [](int grid, const P &p) { k_tree<0><<<grid, 256>>>(p); });
