@@ -82,6 +82,16 @@ struct __align__(16) float8 {
   float4 a, b;
 };
 struct F8 {};  // accumulator tag: fp32, 8 elements per vector
+// fp32, 8 elements per vector moved as ONE 32-byte access (sm_100
+// LDG.E.256 / STG.E.256): every pointer 32-byte aligned, fp32 inputs only.
+// F8WS stores with .cs (evict-first streaming).  The straight-line DIRECT
+// programs of the HBM-bound folds (the N=1 commit, the pre-reduce forests)
+// run on it: tools/hbm_probe.cu measured 6.16 -> 6.7+ TB/s on the 32:8 mix.
+struct F8W {};
+struct F8WS {};
+template <typename A> struct IsW256 { static constexpr bool value = false; };
+template <> struct IsW256<F8W> { static constexpr bool value = true; };
+template <> struct IsW256<F8WS> { static constexpr bool value = true; };
 
 template <typename A> struct VecT;
 template <> struct VecT<float> {
@@ -102,6 +112,8 @@ template <> struct VecT<F8> {
   static constexpr int OUT = 32;
   __host__ __device__ static constexpr int in_bytes(bool bf16) { return bf16 ? 16 : 32; }
 };
+template <> struct VecT<F8W> : VecT<F8> {};
+template <> struct VecT<F8WS> : VecT<F8> {};
 
 __device__ __forceinline__ float4 vadd(const float4 &a, const float4 &b) {
   return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y),
@@ -159,7 +171,14 @@ __device__ __forceinline__ float4 bf16x4_to_f4(uint2 raw) {
 template <typename A>
 __device__ __forceinline__ typename VecT<A>::V ld_vec(const char *p,
                                                       bool bf16) {
-  if constexpr (std::is_same<A, F8>::value) {
+  if constexpr (IsW256<A>::value) {
+    float8 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v.a.x), "=f"(v.a.y), "=f"(v.a.z), "=f"(v.a.w), "=f"(v.b.x), "=f"(v.b.y),
+                   "=f"(v.b.z), "=f"(v.b.w)
+                 : "l"(p));
+    return v;
+  } else if constexpr (std::is_same<A, F8>::value) {
     if (bf16) {  // 8 bf16 in one 16-byte load
       uint4 raw;
       asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -220,6 +239,20 @@ template <typename V> __device__ __forceinline__ void st_vec(char *p, const V &v
 __device__ __forceinline__ void st_vec(char *p, const float8 &v) {
   *reinterpret_cast<float4 *>(p) = v.a;
   *reinterpret_cast<float4 *>(p + 16) = v.b;
+}
+
+// one 32-byte store (F8W) or one streaming 32-byte store (F8WS)
+template <typename A>
+__device__ __forceinline__ void st_w256(char *p, const float8 &v) {
+  if constexpr (std::is_same<A, F8WS>::value) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v.a.x),
+                 "f"(v.a.y), "f"(v.a.z), "f"(v.a.w), "f"(v.b.x), "f"(v.b.y), "f"(v.b.z), "f"(v.b.w)
+                 : "memory");
+  } else {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v.a.x),
+                 "f"(v.a.y), "f"(v.a.z), "f"(v.a.w), "f"(v.b.x), "f"(v.b.y), "f"(v.b.z), "f"(v.b.w)
+                 : "memory");
+  }
 }
 
 // Stores through an NVLink SHARP multicast address (a cuMulticast object
@@ -460,9 +493,18 @@ template <typename Prog> struct IsMulti<Prog, decltype(void(Prog::kMulti))> {
 
 // Evaluate and store one vector position: single-result programs write the
 // (scaled) result to every output, multi-root programs one root per output.
-template <typename Prog, typename V, typename Ld>
+template <typename A, typename Prog, typename V, typename Ld>
 __device__ __forceinline__ void emit(const FoldParams &p, const Ld &ld, unsigned long long off) {
-  if constexpr (IsMulti<Prog>::value) {
+  if constexpr (IsW256<A>::value) {
+    // 256-bit path: straight-line programs, plain (never multicast) outputs
+    if constexpr (IsMulti<Prog>::value) {
+      Prog::template run<V>(p, ld, [&](int j, V r) { st_w256<A>(p.out[j] + off, r); });
+    } else {
+      V r = Prog::template eval<V>(p, ld);
+      if (p.divisor != 0.0) r = vdiv(r, p.divisor);
+      for (int j = 0; j < p.n_out; ++j) st_w256<A>(p.out[j] + off, r);
+    }
+  } else if constexpr (IsMulti<Prog>::value) {
     Prog::template run<V>(p, ld, [&](int j, V r) { st_out(p, j, off, r); });
   } else {
     V r = Prog::template eval<V>(p, ld);
@@ -499,7 +541,7 @@ __global__ void __launch_bounds__(256)
       const bool b = p.bf16[i];
       return ld_vec<A>(p.in[i] + v * (unsigned long long)VecT<A>::in_bytes(b), b);
     };
-    emit<Prog, V>(p, ld, v * (unsigned long long)VecT<A>::OUT);
+    emit<A, Prog, V>(p, ld, v * (unsigned long long)VecT<A>::OUT);
   }
   // only the programs a multicast combine runs DIRECT carry the fence: in the
   // N=1 commit's ProgFull<5> it costs 18 registers (46 -> 64)
@@ -657,7 +699,7 @@ __global__ void __launch_bounds__(TMA_THREADS)
         const bool b = p.bf16[i];
         return lds_vec<A>(stage + p.smem_off[i] + (size_t)vi * VecT<A>::in_bytes(b), b);
       };
-      emit<Prog, V>(p, ld, (v0 + vi) * (unsigned long long)VecT<A>::OUT);
+      emit<A, Prog, V>(p, ld, (v0 + vi) * (unsigned long long)VecT<A>::OUT);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -1263,6 +1305,46 @@ int launch_vec(const FoldReq &r, bool tma, const TmaGeom &g, int maxd,
   return set_err(RCV_ERANGE, "fold program stack depth %d exceeds 8", maxd);
 }
 
+// head elements h (< 8) after which every pointer is 32-byte aligned, or -1
+int common_head32(const FoldReq &r) {
+  for (int h = 0; h < 8; ++h) {
+    bool ok = true;
+    for (int i = 0; i < r.n_in && ok; ++i)
+      ok = ((uintptr_t)(r.in[i] + (size_t)h * esize(r.in_dt[i])) & 31) == 0;
+    for (int j = 0; j < r.n_out && ok; ++j)
+      ok = ((uintptr_t)(r.out[j] + (size_t)h * esize(r.acc_dt)) & 31) == 0;
+    if (ok) return h;
+  }
+  return -1;
+}
+
+// The 256-bit DIRECT launch of a straight-line program (A = F8W / F8WS).
+template <typename A>
+int launch_w256(const FoldReq &r, unsigned long long e0, unsigned long long nvec, cudaStream_t st,
+                int sms) {
+  if (r.n_roots > 0) return launch_direct_p<A, ProgForest>(r, e0, nvec, st, sms);
+  switch (r.full_L) {
+    case 0: return launch_direct_p<A, ProgFull<0>>(r, e0, nvec, st, sms);
+    case 1: return launch_direct_p<A, ProgFull<1>>(r, e0, nvec, st, sms);
+    case 2: return launch_direct_p<A, ProgFull<2>>(r, e0, nvec, st, sms);
+    case 3: return launch_direct_p<A, ProgFull<3>>(r, e0, nvec, st, sms);
+    case 4: return launch_direct_p<A, ProgFull<4>>(r, e0, nvec, st, sms);
+    case 5: return launch_direct_p<A, ProgFull<5>>(r, e0, nvec, st, sms);
+    case 6: return launch_direct_p<A, ProgFull<6>>(r, e0, nvec, st, sms);
+    default: return set_err(RCV_ERANGE, "256-bit path: perfect tree height %d", r.full_L);
+  }
+}
+
+// RCV_W256: 0 off, 1 32-byte loads and stores, 2 the same with streaming
+// (.cs) stores
+int w256_mode() {
+  static const int mode = [] {
+    const char *v = getenv("RCV_W256");
+    return v ? atoi(v) : 2;
+  }();
+  return mode;
+}
+
 // head elements h (< 8) after which every pointer is 16-byte aligned, or -1
 int common_head(const FoldReq &r) {
   for (int h = 0; h < 8; ++h) {
@@ -1289,7 +1371,31 @@ int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int s
   }
   const bool f64 = r.acc_dt == RCV_F64;
   bool wide = r.wide32 && !f64;  // fp32 over bf16 inputs: 8-element vectors (float8)
-  for (int i = 0; i < r.n_in && !f64; ++i) wide |= r.in_dt[i] == RCV_BF16;
+  bool any_bf16 = false;
+  for (int i = 0; i < r.n_in && !f64; ++i) any_bf16 |= r.in_dt[i] == RCV_BF16;
+  wide |= any_bf16;
+  // HBM-bound straight-line folds over fp32 (the N=1 commit's perfect tree,
+  // the pre-reduce forests): 32-byte vectors, one LDG/STG.256 per input and
+  // output (not the NVLink combines, which keep the two-vector pair kernel)
+  if (w256_mode() && !f64 && !any_bf16 && !r.mc_mask && !r.pair &&
+      (variant == RCV_VARIANT_AUTO || variant == RCV_VARIANT_DIRECT) &&
+      ((r.full_L >= 0 && r.full_L <= 6) || r.n_roots > 0)) {
+    const int h32 = common_head32(r);
+    if (h32 >= 0 && (size_t)h32 < numel && (r.n_roots == 0 || (h32 == 0 && numel % 8 == 0))) {
+      const unsigned long long nv = (numel - h32) / 8;
+      const unsigned long long end = h32 + nv * 8;
+      if (h32) {
+        rc = launch_scalar<float>(r, maxd, 0, h32, st, sms);
+        if (rc) return rc;
+      }
+      if (nv) {
+        rc = w256_mode() == 2 ? launch_w256<F8WS>(r, h32, nv, st, sms) : launch_w256<F8W>(r, h32, nv, st, sms);
+        if (rc) return rc;
+      }
+      if (end < numel) rc = launch_scalar<float>(r, maxd, end, numel - end, st, sms);
+      return rc;
+    }
+  }
   const int E = f64 ? 2 : (wide ? 8 : 4);
   int h = variant == RCV_VARIANT_SCALAR ? -1 : common_head(r);
   if (r.n_roots > 0 && (h != 0 || (numel % (2 * E)) != 0))
