@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--no-fail", action="store_true")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--combine-variant", type=int, default=0)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--cpu-sample", type=int, default=1 << 23)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--trace", default="", help="torch.profiler chrome trace prefix (diagnostics)")
@@ -627,7 +627,8 @@ def e2e_leg(args, dev, leaves, numel, world=1):
     """The same step through the public API with HOST inputs: every step each
     rank copies its replicas' microbatch gradients host->device (pinned) and
     its committed gradient device->host, inside the timed region (max over
-    ranks).  Failure-free steps: the host copies are the subject here."""
+    ranks).  Under the same failure schedule as the headline: replica 3 dies
+    during_sync on bucket 7 of the middle timed step (a fresh engine)."""
     import torch
     from paper_2605_11215_b200.commit import GradientCommit
     if world > 1:
@@ -650,10 +651,14 @@ def e2e_leg(args, dev, leaves, numel, world=1):
     out_host = torch.empty(numel, dtype=torch.float32, pin_memory=pinned)
     stream = torch.cuda.current_stream(dev)
 
+    kill = StepKill(-1 if args.no_fail else 1 + args.e2e_steps // 2,
+                    min(VICTIM_BUCKET, args.buckets - 1))
+
     def one(s):
         for m in idx:
             leaves[m].copy_(host[m], non_blocking=True)
-        eng.step(s, lambda m, rid: leaves[m])
+        kill.step = s
+        eng.step(s, lambda m, rid: leaves[m], kill)
         out_host.copy_(eng.grads[mine[0]], non_blocking=True)
 
     one(0)
@@ -677,6 +682,8 @@ def e2e_leg(args, dev, leaves, numel, world=1):
     return {"value": M * TOKENS_PER_MB / (ms / 1e3), "unit": "tokens/s",
             "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "ms_per_step": ms,
             "steps": args.e2e_steps, "pinned": pinned,
+            "failure": None if args.no_fail else "replica 3 during_sync:%d at timed step %d"
+            % (min(VICTIM_BUCKET, args.buckets - 1), args.e2e_steps // 2),
             "pcie_gbs_per_gpu": (bi + bo) / world / (ms / 1e3) / 1e9}
 
 

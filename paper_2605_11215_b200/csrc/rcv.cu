@@ -1377,7 +1377,8 @@ int run_fold(const FoldReq &r, size_t numel, int variant, cudaStream_t st, int s
   // HBM-bound straight-line folds over fp32 (the N=1 commit's perfect tree,
   // the pre-reduce forests): 32-byte vectors, one LDG/STG.256 per input and
   // output (not the NVLink combines, which keep the two-vector pair kernel)
-  if (w256_mode() && !f64 && !any_bf16 && !r.mc_mask && !r.pair &&
+  static const bool w256_comb = getenv("RCV_W256_COMB") && atoi(getenv("RCV_W256_COMB"));
+  if (w256_mode() && !f64 && !any_bf16 && !r.mc_mask && (!r.pair || w256_comb) &&
       (variant == RCV_VARIANT_AUTO || variant == RCV_VARIANT_DIRECT) &&
       ((r.full_L >= 0 && r.full_L <= 6) || r.n_roots > 0)) {
     const int h32 = common_head32(r);
@@ -2799,6 +2800,7 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
     r.op[0] = 0;
     r.n_out = d->n_bcast;
     for (int j = 0; j < d->n_bcast; ++j) r.out[j] = (char *)d->bcast_out[j];
+    r.full_L = 0;  // a one-leaf tree: the straight-line DIRECT (256-bit) copy
     r.acc_dt = d->acc_dtype;
     r.max_ctas = env_ctas("RCV_BCAST_CTAS", ctx->sms, 0.0);
     p->has_bcast = true;
