@@ -462,6 +462,12 @@ def run_ours(args):
     committed = sum(o.contrib_total for o in outcomes)
     tokens = committed * TOKENS_PER_MB
     value = tokens / (elapsed_ms / 1e3)
+    # the paper's effective throughput: processed tokens /
+    # (runtime x alive GPUs), each step weighted by the GPUs still holding a
+    # live replica at its end
+    per = W // world
+    gpu_s = sum(ms / 1e3 * len({rid // per for rid in o.contributions})
+                for ms, o in zip(step_ms, outcomes))
     fail_idx = [i for i, o in enumerate(outcomes) if o.events]
     recovery = recovery_breakdown(eng) if fail_idx else None
     if recovery is not None:
@@ -526,6 +532,7 @@ def run_ours(args):
         # masked-allreduce algorithmic bandwidth: gradient bytes committed
         # (reduced over the live replicas and scaled) per second of step time
         "allreduce_algbw_gbs": numel * 4 / (elapsed_ms / args.steps / 1e3) / 1e9,
+        "effective_tokens_per_s_per_alive_gpu": tokens / gpu_s if gpu_s else None,
         "recovery_ms": recovery["total_ms"] if recovery else None,
         "recovery": recovery,
         "step_ms": {"median": statistics.median(step_ms), "max": max(step_ms),
