@@ -623,10 +623,14 @@ def roofline(dom, per_kind, peak, peak_kind, world=1):
                           "shapes.inc, see kernels_degraded)" % max(0, world.bit_length() - 1),
                 "mean_launch_us": k["mean_launch_us"], "launches_timed": k["launches"],
                 "hbm_gbs": k["hbm_gbs"]}
+    # the accumulator type the library picks for the N=1 commit's perfect
+    # tree (librcv's RCV_W256: 2 = 256-bit vectors with streaming stores)
+    acc = {"0": "float", "1": "F8W"}.get(os.environ.get("RCV_W256", "2"), "F8WS")
+    name = "fold_direct_kernel<%s, ProgFull<5>>" % acc
     return {"bound": "hbm", "achieved": k["hbm_gbs"], "peak": peak, "unit": "GB/s",
             "frac": k["hbm_gbs"] / peak if k["hbm_gbs"] else None,
-            "traffic": traffic_of("fold_direct_kernel<float, ProgFull<5>>"), "peak_kind": peak_kind,
-            "kernel": "fold_direct_kernel<float, ProgFull<L>> (rcv_tree_commit AUTO, %s)" % dom,
+            "traffic": traffic_of(name), "peak_kind": peak_kind,
+            "kernel": "%s (rcv_tree_commit AUTO, %s)" % (name, dom),
             "mean_launch_us": k["mean_launch_us"], "launches_timed": k["launches"]}
 
 
