@@ -440,6 +440,7 @@ def run_ours(args):
         start.record(stream)
         t_host = time.perf_counter()
         host_step = []
+        prof0 = dict(getattr(eng, "host_prof", {}))
         for s in range(args.warmup, total_steps):
             kill.step = s
             a = torch.cuda.Event(enable_timing=True)
@@ -541,6 +542,11 @@ def run_ours(args):
                     "degraded_median": statistics.median(post) if post else None,
                     "all": [round(x, 3) for x in step_ms]},
         "host_enqueue_ms_per_step": host_ms,
+        # where the host time goes (multi-process engine): plan lookup/build,
+        # the native per-bucket enqueue, the wait for the previous step's
+        # status words (the GPU running behind the host)
+        "host_prof_ms_per_step": {k: (v - prof0.get(k, 0.0)) * 1e3 / args.steps
+                                  for k, v in getattr(eng, "host_prof", {}).items()} or None,
         # host time inside eng.step (control plane + launches): a step whose
         # host time exceeds its device time leaves the GPU waiting
         "host_step_ms": {"failure_free_median": statistics.median(host_step[:fail_idx[0]])

@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+from collections import OrderedDict
 from typing import Optional, Sequence
 
 import torch
@@ -481,13 +482,33 @@ class BucketRuntime:
         self.ctx = h
         self.plan = None
         self._keep = None
+        # native plans by leaf layout: a failure-free step reuses the plan of
+        # the step before it instead of rebuilding it (host time per step)
+        self._cache: "OrderedDict" = OrderedDict()
+        self.cache_size = 8
 
-    def set_plan(self, desc: "PlanDesc", keep) -> None:
+    def set_plan(self, desc: "PlanDesc", keep, key=None) -> None:
         h = ctypes.c_void_p(0)
         _check(load().rcv_plan_create(self.ctx, ctypes.byref(desc), ctypes.byref(h)))
-        if self.plan is not None:
-            load().rcv_plan_destroy(self.plan)
+        if key is None:
+            if self.plan is not None and not any(v[0] is self.plan for v in self._cache.values()):
+                load().rcv_plan_destroy(self.plan)
+            self.plan, self._keep = h, keep
+            return
+        self._cache[key] = (h, keep)
         self.plan, self._keep = h, keep
+        while len(self._cache) > self.cache_size:
+            _, (old, _) = self._cache.popitem(last=False)
+            load().rcv_plan_destroy(old)
+
+    def use_cached(self, key) -> bool:
+        """Make the cached plan of `key` current; False when there is none."""
+        hit = self._cache.get(key)
+        if hit is None:
+            return False
+        self._cache.move_to_end(key)
+        self.plan, self._keep = hit
+        return True
 
     def bucket(self, lo: int, n: int, stream: int) -> None:
         _check(load().rcv_plan_bucket(self.plan, lo, n, stream))
@@ -516,6 +537,10 @@ class BucketRuntime:
 
     def close(self) -> None:
         lib = load()
+        for h, _ in self._cache.values():
+            if h is not self.plan:
+                lib.rcv_plan_destroy(h)
+        self._cache.clear()
         if self.plan is not None:
             lib.rcv_plan_destroy(self.plan)
             self.plan = None

@@ -39,6 +39,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 
 import ctypes
 import os
+import time
 
 import torch
 import torch.distributed as dist
@@ -451,6 +452,10 @@ class DistributedGradientCommit(GradientCommit):
                     pass
             self.rt.set_liveness(self.liveness)
         self._plan_key = None
+        self._stream: Optional[int] = None
+        # host seconds spent building/looking up plans, enqueueing buckets and
+        # waiting for the previous step's status words (bench.py reports them)
+        self.host_prof = {"plan_s": 0.0, "bucket_s": 0.0, "wait_s": 0.0}
         torch.cuda.synchronize(self.device)
         dist.barrier(group=group)
 
@@ -563,11 +568,14 @@ class DistributedGradientCommit(GradientCommit):
     def _end_of_step(self) -> None:
         ranks, mask = self._live_mask()
         stream = torch.cuda.current_stream(self.device)
+        self._stream = None  # looked up again at the next step's first bucket
         self.rt.finish(mask, self.rank in ranks, stream.cuda_stream)
         # the previous step's snapshot is complete by now (a step ago);
         # check it, then snapshot this step's words behind its last kernel
         if self._status_ev is not None:
+            h0 = time.perf_counter()
             self._status_ev.synchronize()
+            self.host_prof["wait_s"] += time.perf_counter() - h0
             self._judge(self._status_host.tolist(), "a previous step")
         self._status_host.copy_(self.status, non_blocking=True)
         self._status_ev = torch.cuda.Event()
@@ -609,7 +617,7 @@ class DistributedGradientCommit(GradientCommit):
         self.rt.set_timing(False)
         return out
 
-    def _set_plan(self, leaves) -> None:
+    def _set_plan(self, leaves, layout=None) -> None:
         """Build the native plan of a leaf set: local pre-reduce nodes, the
         combine over every cover node's pool slot, the local broadcast."""
         b = self.state.b
@@ -671,7 +679,7 @@ class DistributedGradientCommit(GradientCommit):
             remote_in=sum(1 for rk, _ in slot_of.values() if rk != self.rank),
             remote_out=n_remote_out,
             guarded=int(self.real_kill), comb_out_mc=int(self.multicast))
-        self.rt.set_plan(d, keep)
+        self.rt.set_plan(d, keep, layout)
 
     def _reduce_bucket(self, k: int, leaves) -> int:
         lo, hi = self.bounds[k]
@@ -685,9 +693,21 @@ class DistributedGradientCommit(GradientCommit):
             return 1
         key = (id(leaves), tuple(self.comm.members))
         if self._plan_key is None or self._plan_key[0] != key or self._plan_key[1] is not leaves:
-            self._set_plan(leaves)
+            h0 = time.perf_counter()
+            # the native plan depends only on the leaf layout: which rank
+            # holds which microbatch at which address, and the membership
+            layout = (tuple(self.comm.members), self.state.b,
+                      tuple((m, rid, v.data_ptr(), v.dtype) if v is not None else (m, rid)
+                            for m, (rid, v) in sorted(leaves.items())))
+            if not self.rt.use_cached(layout):
+                self._set_plan(leaves, layout)
             self._plan_key = (key, leaves)
-        self.rt.bucket(lo, n, torch.cuda.current_stream(self.device).cuda_stream)
+            self.host_prof["plan_s"] += time.perf_counter() - h0
+        if self._stream is None:
+            self._stream = torch.cuda.current_stream(self.device).cuda_stream
+        h0 = time.perf_counter()
+        self.rt.bucket(lo, n, self._stream)
+        self.host_prof["bucket_s"] += time.perf_counter() - h0
         return 1
 
 
