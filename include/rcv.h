@@ -273,32 +273,44 @@ int rcv_barrier(uint64_t *local_flags, void *const *peer_flags, int n, int me,
                 uint32_t *status, void *stream);
 
 /* ---- native per-bucket runtime for the multi-process commit --------------
- * One context per rank (flags, status, a side stream for pre-reduces, the
- * barrier sequence, the pending local broadcasts); one plan per leaf cover
- * (prepared fold requests: validated once, relaunched per bucket).  A bucket
- * call j then costs the host one call: rcv_plan_bucket enqueues
- *   main stream:  [membership shrank since the previous call: barrier over
- *                 the previous live mask, departing ranks included] ->
- *   side stream:  wait(barrier j-2: pool set j%3 free) -> [broadcasts,
+ * One context per rank (flags, status, side / barrier / broadcast streams,
+ * the barrier sequence, the pending local broadcasts); one plan per leaf
+ * cover (prepared fold requests: validated once, relaunched per bucket).  A
+ * bucket call j then costs the host one call: rcv_plan_bucket enqueues, with
+ * barrier lag L (RCV_BARRIER_LAG, default 2)
+ *   [membership shrank since the previous call: barrier over the previous
+ *    live mask behind this rank's last combine, departing ranks included]
+ *   side stream:  wait(barrier j-S+L: pool set j%S free) -> [broadcasts,
  *                 fragmented covers] -> stamp(set) = 0 -> pre-reduce nodes
- *                 into pool set j%3 -> stamp(set) = j+1 -> record(ready)
- *   main stream:  wait(ready) -> barrier -> record(arrived) ->
- *                 combine(owner slice; checks every producer's stamp == j+1
- *                 before its first and after its last load)
- *   bcast stream: wait(arrived) -> broadcasts of the buckets combined before
- *                 (perfect covers: one node per live rank)
- * and rcv_ctx_finish closes the step (barrier + last broadcasts).
+ *                 into pool set j%S -> stamp(set) = j+1 -> record(ready)
+ *   bar stream:   wait(ready) -> wait(combine j-L) -> barrier (before its
+ *                 signal re-checks the stamps combine j-L read; after its
+ *                 wait checks every producer's stamp of set j%S == j+1)
+ *                 -> record(arrived)
+ *   main stream:  wait(arrived) -> combine(owner slice) -> record(combined)
+ *   bcast stream: wait(arrived) -> broadcasts of the buckets combined at
+ *                 calls <= j-L (perfect covers: one node per live rank)
+ * With L = 2 barrier j overlaps combine j-1, so the combines run back to
+ * back; L = 1 is the serial barrier -> combine order.
+ * rcv_ctx_finish closes the step (barrier behind every combine + last
+ * broadcasts).
  * rcv_ctx_create loads every kernel of the library up front (CUDA lazy
  * loading could otherwise need a context sync while a kernel waits on a
  * peer's flag).
+ * S = rcv_pool_sets() partial-pool sets, allocated by the caller
+ * (plan set_stride apart).
  * local_flags / peer_flags: 128 uint64 per rank ([0,64) barrier sequence per
- * peer, [64,67) pool-set stamps).
+ * peer, [64,64+S) pool-set stamps).
  * status: two uint32 words: [0] peers that timed out (bit per rank),
  * [1] stamp mismatches seen by this rank's combines (bit 0: a partial was
  * not ready, bit 1: it was overwritten while being read).  Nonzero word 1
  * means the committed bits of that step are not trustworthy. */
 typedef struct rcv_ctx rcv_ctx;
 typedef struct rcv_plan rcv_plan;
+
+/* Number S of partial-pool sets a context rotates through (4; the
+ * RCV_POOL_SETS=3 measurement switch gives 3). */
+int rcv_pool_sets(void);
 
 int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags,
                    void *const *peer_flags, uint32_t *status,
@@ -307,8 +319,9 @@ int rcv_ctx_destroy(rcv_ctx *ctx);
 int rcv_ctx_finish(rcv_ctx *ctx, uint64_t live_mask, int participate,
                    void *main_stream);
 int rcv_ctx_set_timing(rcv_ctx *ctx, int on);
-/* A barrier over live_mask on main_stream behind everything this context
- * enqueued (side and broadcast streams joined), outside the bucket sequence:
+/* A barrier over live_mask behind everything this context enqueued (side
+ * and broadcast streams joined; main_stream waits for it), outside the
+ * bucket sequence:
  * the real-kill protocol's synchronisation point before it decides a step
  * (a departed rank of the previous mask joins it, as for a bucket call). */
 int rcv_ctx_poll(rcv_ctx *ctx, uint64_t live_mask, int participate, void *main_stream);

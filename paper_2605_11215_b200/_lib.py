@@ -38,6 +38,7 @@ EXPORTS = (
     "rcv_liveness_stats", "rcv_liveness_note_kill", "rcv_liveness_destroy",
     "rcv_mc_supported", "rcv_mc_granularity", "rcv_mc_create", "rcv_mc_import",
     "rcv_mc_add_device", "rcv_mc_bind", "rcv_mc_map", "rcv_mc_release",
+    "rcv_pool_sets",
 )
 
 
@@ -121,6 +122,7 @@ def load() -> ctypes.CDLL:
         "rcv_tree_commit_at": (i32, [ctypes.POINTER(_Block), i32, u32, i32, pvp,
                                      i32, sz, sz, sz, ctypes.c_double, i32, vp]),
         "rcv_ctx_create": (i32, [i32, i32, vp, pvp, vp, u64, ctypes.POINTER(vp)]),
+        "rcv_pool_sets": (i32, []),
         "rcv_ctx_destroy": (i32, [vp]),
         "rcv_ctx_finish": (i32, [vp, u64, i32, vp]),
         "rcv_ctx_set_timing": (i32, [vp, i32]),
@@ -465,6 +467,11 @@ class TreePlan:
 
 
 KIND_NAMES = ("prereduce", "barrier", "broadcast", "combine")
+
+
+def pool_sets() -> int:
+    """Partial-pool sets the native runtime rotates through (rcv_pool_sets)."""
+    return int(load().rcv_pool_sets())
 
 
 class BucketRuntime:

@@ -960,8 +960,9 @@ struct BarrierParams {
   // i.e. started overwriting a partial, before that combine had finished)
   const unsigned long long *chk_now[32];
   const unsigned long long *chk_prev[32];
+  unsigned long long prev_value[32];  // per entry: earlier combines read different calls' sets
   int n_now, n_prev;
-  unsigned long long now_value, prev_value;
+  unsigned long long now_value;
   unsigned int *err;
   // real-kill mode: the node's liveness dead word (mapped host memory,
   // rcv_liveness); a peer whose bit is set is not waited for
@@ -970,14 +971,15 @@ struct BarrierParams {
 
 __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   const int t = threadIdx.x;
-  // the previous combine on this stream has finished (kernel order): its
-  // producers' stamps must still be that call's.  Checked before this rank
-  // signals: no producer may rewrite that pool set before it has seen this
-  // rank arrive here, so a changed stamp means a real overwrite race.
+  // the combines listed in chk_prev have finished (the host ordered this
+  // launch behind them): their producers' stamps must still be those calls'.
+  // Checked before this rank signals: no producer may rewrite such a pool
+  // set before it has seen this rank arrive here, so a changed stamp means a
+  // real overwrite race.
   if (t < p.n_prev) {
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.chk_prev[t]) : "memory");
-    if (v != p.prev_value) atomicOr(p.err, 2u);
+    if (v != p.prev_value[t]) atomicOr(p.err, 2u);
   }
   // a peer that already timed out is dead: never signal or wait on it again
   const unsigned int dead = *(volatile const unsigned int *)p.status | (p.host_dead ? *p.host_dead : 0u);
@@ -1012,6 +1014,120 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.chk_now[t]) : "memory");
     if (v != p.now_value) atomicOr(p.err, 1u);
   }
+}
+
+// ---------------------------------------------------------------------------
+// drop-in multi-device collective in one launch per device (single process,
+// one view per replica on several GPUs): entry flag barrier, this device's
+// owner slice of the ascending masked fold (ref:comm.py:191-200), exit flag
+// barrier, fused so a small bucket costs one launch per device instead of
+// three.  Flags are the device group's (MdGroup): slot `me` of every peer's
+// array receives this device's sequence numbers.
+
+constexpr int kMdMaxIn = 8;  // contributors evaluated from registers
+
+struct MdParams {
+  const char *in[kMdMaxIn];
+  char *out[RCV_MAX_OUT];
+  int n_in, n_out;
+  unsigned long long nvec;  // whole vectors of the owner slice
+  unsigned long long tail;  // trailing scalars (ragged last slice)
+  double divisor;           // 0: no scale
+  unsigned long long *peer[32];
+  unsigned long long *local;
+  unsigned int *status;
+  unsigned int *count;  // blocks done (reset by the last one)
+  unsigned long long v_in, v_out, timeout_ns;
+  int n_dev, me;
+};
+
+__device__ __forceinline__ void md_wait(const MdParams &p, int t, unsigned long long v) {
+  if (t < p.n_dev && t != p.me) {
+    const unsigned long long t0 = globaltimer();
+    unsigned long long x;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(p.local + t) : "memory");
+      if (x >= v) break;
+      if (globaltimer() - t0 > p.timeout_ns) {
+        atomicOr(p.status, 1u << (t & 31));
+        break;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void md_signal(const MdParams &p, int t, unsigned long long v) {
+  if (t < p.n_dev && t != p.me)
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.peer[t] + p.me), "l"(v) : "memory");
+}
+
+template <typename T> struct MdVec;
+template <> struct MdVec<float> { typedef float4 V; };
+template <> struct MdVec<double> { typedef double2 V; };
+
+// coherent 16-byte load (the peers' views were written before their entry
+// signal, which this thread's block acquired)
+__device__ __forceinline__ float4 md_ld(const char *a, float4 *) {
+  float4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ double2 md_ld(const char *a, double2 *) {
+  double2 v;
+  asm volatile("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(a) : "memory");
+  return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) md_allreduce_kernel(const __grid_constant__ MdParams p) {
+  typedef typename MdVec<T>::V V;
+  const int t = threadIdx.x;
+  __shared__ int last;
+  if (blockIdx.x == 0) {
+    // this device's earlier stream work (the contributors' accumulation) is
+    // complete: release it to the peers
+    __threadfence_system();
+    md_signal(p, t, p.v_in);
+  }
+  md_wait(p, t, p.v_in);
+  __syncthreads();
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + t; i < p.nvec; i += stride) {
+    const unsigned long long off = i * sizeof(V);
+    V x[kMdMaxIn];
+#pragma unroll
+    for (int k = 0; k < kMdMaxIn; ++k)
+      if (k < p.n_in) x[k] = md_ld(p.in[k] + off, (V *)nullptr);
+    V acc = x[0];
+#pragma unroll
+    for (int k = 1; k < kMdMaxIn; ++k)
+      if (k < p.n_in) acc = vadd(acc, x[k]);
+    if (p.divisor != 0.0) acc = vdiv(acc, p.divisor);
+    for (int j = 0; j < p.n_out; ++j) *reinterpret_cast<V *>(p.out[j] + off) = acc;
+  }
+  if (blockIdx.x == 0 && t < (int)p.tail) {
+    const unsigned long long off = p.nvec * sizeof(V) + (unsigned long long)t * sizeof(T);
+    T acc = *reinterpret_cast<const volatile T *>(p.in[0] + off);
+    for (int k = 1; k < p.n_in; ++k) acc = sadd(acc, *reinterpret_cast<const volatile T *>(p.in[k] + off));
+    if (p.divisor != 0.0) acc = sdiv(acc, p.divisor);
+    for (int j = 0; j < p.n_out; ++j) *reinterpret_cast<T *>(p.out[j] + off) = acc;
+  }
+  // exit: the last block to finish tells the peers that every store of this
+  // device's slice has landed, then waits until theirs have (this launch
+  // completes only when every remote store into this device's views is done)
+  __threadfence_system();
+  __syncthreads();
+  if (t == 0) {
+    const unsigned int done = atomicAdd(p.count, 1u);
+    last = done == gridDim.x - 1;
+    if (last) *p.count = 0;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence_system();
+  md_signal(p, t, p.v_out);
+  md_wait(p, t, p.v_out);
 }
 
 // ---------------------------------------------------------------------------
@@ -1592,6 +1708,7 @@ struct MdGroup {
   std::vector<int> devs;
   std::vector<unsigned long long *> flags;
   std::vector<unsigned int *> status;
+  std::vector<unsigned int *> count;  // md_allreduce_kernel's finished-block counter
   unsigned long long seq = 0;
 };
 std::mutex g_md_mu;
@@ -1611,11 +1728,12 @@ int md_group(const int *devices, int n, MdGroup **out) {
     unsigned int *s = nullptr;
     CK(cudaMalloc(&f, 64 * sizeof(unsigned long long)));
     CK(cudaMemset(f, 0, 64 * sizeof(unsigned long long)));
-    CK(cudaMalloc(&s, sizeof(unsigned int)));
-    CK(cudaMemset(s, 0, sizeof(unsigned int)));
+    CK(cudaMalloc(&s, 2 * sizeof(unsigned int)));
+    CK(cudaMemset(s, 0, 2 * sizeof(unsigned int)));
     g->devs.push_back(devices[d]);
     g->flags.push_back(f);
     g->status.push_back(s);
+    g->count.push_back(s + 1);
   }
   CK(cudaDeviceSynchronize());
   g_md.push_back(g);
@@ -1640,6 +1758,59 @@ int md_barrier(MdGroup *g, int d, cudaStream_t st, unsigned long long value) {
   CK(cudaGetLastError());
   return RCV_OK;
 }
+// The fused one-launch path: fp32/fp64 views, at most kMdMaxIn
+// contributors, 16-byte aligned views (RCV_MD_SPLIT=1: the three-launch
+// path, a measurement A/B).
+bool md_fused_ok(const FoldReq &r, void *const *views, int n) {
+  static const bool split = getenv("RCV_MD_SPLIT") && atoi(getenv("RCV_MD_SPLIT"));
+  if (split || r.n_in < 1 || r.n_in > kMdMaxIn || (r.acc_dt != RCV_F32 && r.acc_dt != RCV_F64))
+    return false;
+  for (int i = 0; i < n; ++i)
+    if ((uintptr_t)views[i] % 16) return false;
+  return true;
+}
+
+int md_fused(const FoldReq &r, MdGroup *g, size_t numel, const int *devices, int n_dev,
+             void *const *streams, unsigned long long v_in, unsigned long long v_out) {
+  const int es = esize(r.acc_dt);
+  const size_t w = 16 / es;  // elements per vector
+  const size_t unit = 8;
+  const size_t units = (numel + unit - 1) / unit;
+  MdParams p;
+  memset(&p, 0, sizeof p);
+  p.n_in = r.n_in;
+  p.n_out = r.n_out;
+  p.divisor = r.divisor;
+  p.timeout_ns = 10ull * 1000000000ull;
+  p.n_dev = n_dev;
+  p.v_in = v_in;
+  p.v_out = v_out;
+  for (int k = 0; k < n_dev; ++k) p.peer[k] = g->flags[k];
+  // every device launches, an empty slice included: its peers wait on its flags
+  for (int d = 0; d < n_dev; ++d) {
+    const size_t a = std::min(numel, units * d / n_dev * unit);
+    const size_t b = std::min(numel, units * (d + 1) / n_dev * unit);
+    for (int i = 0; i < r.n_in; ++i) p.in[i] = r.in[i] + a * es;
+    for (int j = 0; j < r.n_out; ++j) p.out[j] = r.out[j] + a * es;
+    p.nvec = (b - a) / w;
+    p.tail = (b - a) % w;
+    p.local = g->flags[d];
+    p.status = g->status[d];
+    p.count = g->count[d];
+    p.me = d;
+    CK(cudaSetDevice(devices[d]));
+    const unsigned long long want = (p.nvec + 255) / 256;
+    const unsigned int blocks = (unsigned int)std::max<unsigned long long>(
+        1, std::min<unsigned long long>(want, 4ull * dev_sms(devices[d])));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (r.acc_dt == RCV_F32)
+      md_allreduce_kernel<float><<<blocks, 256, 0, (cudaStream_t)streams[d]>>>(p);
+    else
+      md_allreduce_kernel<double><<<blocks, 256, 0, (cudaStream_t)streams[d]>>>(p);
+    CK(cudaGetLastError());
+  }
+  return RCV_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -1649,7 +1820,9 @@ extern "C" {
 // entry barrier proves every device's prior stream work (the contributors'
 // accumulation into their views) is done before any peer reads it, the exit
 // barrier that every remote store into this device's views has landed
-// before its stream moves on.
+// before its stream moves on.  fp32/fp64 with <= 8 contributors: all three
+// in one launch per device (md_allreduce_kernel); otherwise barrier, fold
+// kernel, barrier.
 int rcv_masked_allreduce_multidev(void *const *views, int n,
                                   uint64_t contrib_mask, int dtype,
                                   size_t numel, double divisor, int n_dev,
@@ -1664,6 +1837,11 @@ int rcv_masked_allreduce_multidev(void *const *views, int n,
   MdGroup *g = nullptr;
   if ((rc = md_group(devices, n_dev, &g))) return rc;
   const unsigned long long v_in = ++g->seq, v_out = ++g->seq;
+  if (md_fused_ok(r, views, n)) {
+    rc = md_fused(r, g, numel, devices, n_dev, streams, v_in, v_out);
+    cudaSetDevice(prev);
+    return rc;
+  }
   for (int d = 0; d < n_dev; ++d) {
     CK(cudaSetDevice(devices[d]));
     if ((rc = md_barrier(g, d, (cudaStream_t)streams[d], v_in))) return rc;
@@ -2305,8 +2483,9 @@ int rcv_toy_grad(int kind_linear, const double *params, const double *lanes,
 namespace {
 
 // pool-set integrity stamps live in the rank's flag array after the barrier
-// slots: word kStampBase + s belongs to pool set s (three sets)
+// slots: word kStampBase + s belongs to pool set s (rcv_pool_sets() sets)
 constexpr int kStampBase = 64;
+constexpr int kMaxSets = 4;
 
 __global__ void stamp_kernel(unsigned long long *addr, unsigned long long value) {
   __threadfence_system();
@@ -2329,8 +2508,18 @@ struct rcv_ctx {
   unsigned int *err = nullptr;  // status word 1: stamp mismatches seen by this rank's combines
   cudaStream_t side = nullptr;     // pre-reduces (and fragmented covers' broadcasts)
   cudaStream_t bstream = nullptr;  // perfect covers' broadcasts, right behind each barrier
+  cudaStream_t bar_st = nullptr;   // every flag barrier, in call order
   cudaEvent_t ev_main = nullptr, ev_ready = nullptr, ev_trans = nullptr, ev_bcast = nullptr;
-  cudaEvent_t ev_arrived[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_join = nullptr;
+  cudaEvent_t ev_arrived[kMaxSets] = {};  // barrier of call j passed
+  cudaEvent_t ev_comb[kMaxSets] = {};     // combine of call j finished
+  int sets = 4;                           // pool sets rotated through (rcv_pool_sets)
+  // barrier lag L (RCV_BARRIER_LAG, 1 or 2): the barrier of call j runs on
+  // its own stream behind this rank's combine j-L, so with L = 2 it overlaps
+  // combine j-1 and the combines run back to back on the main stream.
+  // Passing barrier j proves every live peer finished its pre-reduce j and
+  // its combine j-L; every other wait in the schedule follows from that.
+  int lag = 2;
   bool in_step = false;
   bool bstream_dirty = false;  // bstream holds broadcasts the side stream has not waited for
   unsigned long long calls = 0, seq = 0;
@@ -2341,9 +2530,13 @@ struct rcv_ctx {
   uint64_t last_live = 0;
   WriteValue64 write_value = nullptr;  // cuStreamWriteValue64 (stamp_kernel when absent)
   bool no_stamps = false;              // RCV_NO_STAMPS=1: measurement A/B only
-  // the stamps the last combine on main read, re-checked by the next barrier
-  std::vector<const unsigned long long *> chk;
-  unsigned long long chk_value = 0;
+  // the stamps each combine not yet re-checked read, in call order; a
+  // barrier re-checks those of the combines it is ordered behind
+  struct Check {
+    unsigned long long call, value;
+    std::vector<const unsigned long long *> stamps;
+  };
+  std::vector<Check> hist;
   struct Pending {
     FoldReq req;
     size_t lo, n;
@@ -2403,31 +2596,40 @@ int timed(rcv_ctx *c, cudaStream_t st, int kind, double bytes, double nin, doubl
   return rc;
 }
 
-// `now`: the stamps the combine launched right behind this barrier reads
-// (checked == now_value after the wait); the previous combine's stamps are
-// re-checked by the same launch (BarrierParams::chk_*).
-int ctx_barrier(rcv_ctx *c, uint64_t live, bool participate, cudaStream_t st,
+// Barriers run on the bar stream (the caller's stream while timing launch
+// by launch).  `upto`: the last call whose combine this barrier is ordered
+// behind (-1: all of them; the caller made the bar stream wait for main's
+// tail); those combines' stamps are re-checked before the signal.  `now`:
+// the stamps the combine of this call reads, checked == now_value after the
+// wait.
+int ctx_barrier(rcv_ctx *c, uint64_t live, bool participate, cudaStream_t st, long long upto,
+                unsigned long long call = 0,
                 const std::vector<const unsigned long long *> *now = nullptr,
                 unsigned long long now_value = 0) {
   if (!participate || __builtin_popcountll(live) < 2) {
-    c->chk.clear();  // no peer: nothing can race this rank's combines
+    c->hist.clear();  // no peer: nothing can race this rank's combines
     return RCV_OK;
   }
   c->bar.live = live;
   c->bar.value = ++c->seq;
   c->bar.err = c->err;
-  c->bar.n_prev = (int)c->chk.size();
-  for (int i = 0; i < c->bar.n_prev; ++i) c->bar.chk_prev[i] = c->chk[i];
-  c->bar.prev_value = c->chk_value;
+  int np = 0;
+  size_t done = 0;
+  for (; done < c->hist.size(); ++done) {
+    const rcv_ctx::Check &h = c->hist[done];
+    if (upto >= 0 && (long long)h.call > upto) break;
+    for (const unsigned long long *a : h.stamps) {
+      if (np == 32) break;
+      c->bar.chk_prev[np] = a;
+      c->bar.prev_value[np++] = h.value;
+    }
+  }
+  c->hist.erase(c->hist.begin(), c->hist.begin() + done);
+  c->bar.n_prev = np;
   c->bar.n_now = now ? (int)now->size() : 0;
   for (int i = 0; i < c->bar.n_now; ++i) c->bar.chk_now[i] = (*now)[i];
   c->bar.now_value = now_value;
-  if (now) {
-    c->chk = *now;
-    c->chk_value = now_value;
-  } else {
-    c->chk.clear();
-  }
+  if (now) c->hist.push_back({call, now_value, *now});
   return timed(c, st, 1, 0, 0, 0, [&]() {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     barrier_kernel<<<1, 32, 0, st>>>(c->bar);
@@ -2436,21 +2638,40 @@ int ctx_barrier(rcv_ctx *c, uint64_t live, bool participate, cudaStream_t st,
   });
 }
 
+cudaStream_t bar_stream(rcv_ctx *c, cudaStream_t main) { return c->timing ? main : c->bar_st; }
+
+// `to` waits for everything enqueued on `from` so far
+int join(rcv_ctx *c, cudaStream_t from, cudaStream_t to) {
+  if (from == to) return RCV_OK;
+  CK(cudaEventRecord(c->ev_join, from));
+  CK(cudaStreamWaitEvent(to, c->ev_join, 0));
+  return RCV_OK;
+}
+
+// A barrier behind all of this rank's work on `main` (closing, poll and
+// transition barriers), then `main`, side and bstream wait for it.
+int full_barrier(rcv_ctx *c, uint64_t live, bool participate, cudaStream_t main) {
+  cudaStream_t b = bar_stream(c, main);
+  int rc = join(c, main, b);
+  if (rc) return rc;
+  if ((rc = ctx_barrier(c, live, participate, b, -1))) return rc;
+  CK(cudaEventRecord(c->ev_trans, b));
+  CK(cudaStreamWaitEvent(main, c->ev_trans, 0));
+  CK(cudaStreamWaitEvent(c->side, c->ev_trans, 0));
+  if (c->bstream) CK(cudaStreamWaitEvent(c->bstream, c->ev_trans, 0));
+  return RCV_OK;
+}
+
 // Membership shrank since the previous call of this step: every rank of the
-// previous mask joins one barrier over it on its main stream, after its last
-// combine.  Passing it proves that the departing ranks' combines, which read
-// this rank's pool sets and stored into its primary replica, are complete,
-// so no pool set is rewritten and no bucket broadcast before they land.
+// previous mask joins one barrier over it, after its last combine.  Passing
+// it proves that the departing ranks' combines, which read this rank's pool
+// sets and stored into its primary replica, are complete, so no pool set is
+// rewritten and no bucket broadcast before they land.
 int ctx_transition(rcv_ctx *c, uint64_t live, cudaStream_t main) {
   const uint64_t prev = c->last_live;
   c->last_live = live;
   if (!prev || !(prev & ~live)) return RCV_OK;
-  int rc = ctx_barrier(c, prev, (prev >> c->me) & 1ull, main);
-  if (rc) return rc;
-  CK(cudaEventRecord(c->ev_trans, main));
-  CK(cudaStreamWaitEvent(c->side, c->ev_trans, 0));
-  if (c->bstream) CK(cudaStreamWaitEvent(c->bstream, c->ev_trans, 0));
-  return RCV_OK;
+  return full_barrier(c, prev, (prev >> c->me) & 1ull, main);
 }
 
 int stamp_write(rcv_ctx *c, cudaStream_t st, unsigned long long *addr, unsigned long long v) {
@@ -2554,6 +2775,13 @@ double comb_share(const rcv_plan_desc *d) {
 
 extern "C" {
 
+int rcv_pool_sets(void) {
+  // RCV_POOL_SETS (3 or 4) is a measurement A/B; the allocator (dist.py)
+  // and the context read the same value
+  const char *v = getenv("RCV_POOL_SETS");
+  return v && atoi(v) == 3 ? 3 : kMaxSets;
+}
+
 int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer_flags,
                    uint32_t *status, uint64_t timeout_ns, rcv_ctx **out) {
   if (n_ranks < 1 || n_ranks > 32 || me < 0 || me >= n_ranks)
@@ -2591,11 +2819,22 @@ int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer
   }
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->bstream, cudaStreamNonBlocking));
+  {
+    // the barrier stream gets the highest priority: its one-CTA kernel must
+    // find a slot while the pre-reduce and combine grids occupy the SMs
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&c->bar_st, cudaStreamNonBlocking, hi));
+  }
+  if (const char *v = getenv("RCV_BARRIER_LAG")) c->lag = atoi(v) == 1 ? 1 : 2;
+  CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  for (int i = 0; i < kMaxSets; ++i) CK(cudaEventCreateWithFlags(&c->ev_comb[i], cudaEventDisableTiming));
+  c->sets = rcv_pool_sets();
   CK(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_trans, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_bcast, cudaEventDisableTiming));
-  for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->ev_arrived[i], cudaEventDisableTiming));
+  for (int i = 0; i < kMaxSets; ++i) CK(cudaEventCreateWithFlags(&c->ev_arrived[i], cudaEventDisableTiming));
   *out = c;
   return RCV_OK;
 }
@@ -2604,13 +2843,19 @@ int rcv_ctx_destroy(rcv_ctx *c) {
   if (!c) return RCV_OK;
   cudaStreamSynchronize(c->side);
   cudaStreamSynchronize(c->bstream);
+  cudaStreamSynchronize(c->bar_st);
   for (auto &r : c->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }
   for (auto e : c->spare_events) cudaEventDestroy(e);
   for (cudaEvent_t e : {c->ev_main, c->ev_ready, c->ev_trans, c->ev_bcast}) cudaEventDestroy(e);
-  for (int i = 0; i < 3; ++i) cudaEventDestroy(c->ev_arrived[i]);
+  cudaEventDestroy(c->ev_join);
+  for (int i = 0; i < kMaxSets; ++i) {
+    cudaEventDestroy(c->ev_arrived[i]);
+    cudaEventDestroy(c->ev_comb[i]);
+  }
+  cudaStreamDestroy(c->bar_st);
   cudaStreamDestroy(c->bstream);
   cudaStreamDestroy(c->side);
   delete c;
@@ -2647,26 +2892,28 @@ int rcv_ctx_timing(rcv_ctx *c, int max, int *kind, float *ms, double *bytes, dou
   return RCV_OK;
 }
 
+// The side and broadcast streams' tails join the caller's stream.
+static int join_tails(rcv_ctx *c, cudaStream_t st, bool clear) {
+  if (!c->in_step) return RCV_OK;
+  int rc = join(c, c->side, st);
+  if (rc) return rc;
+  if (c->bstream_dirty) {
+    if ((rc = join(c, c->bstream, st))) return rc;
+    if (clear) c->bstream_dirty = false;
+  }
+  return RCV_OK;
+}
+
 int rcv_ctx_finish(rcv_ctx *c, uint64_t live_mask, int participate, void *main_stream) {
   cudaStream_t st = (cudaStream_t)main_stream;
-  if (c->in_step) {
-    // the side stream's tail (broadcasts) joins the caller's stream
-    CK(cudaEventRecord(c->ev_ready, c->side));
-    CK(cudaStreamWaitEvent(st, c->ev_ready, 0));
-    if (c->bstream_dirty) {
-      CK(cudaEventRecord(c->ev_ready, c->bstream));
-      CK(cudaStreamWaitEvent(st, c->ev_ready, 0));
-      c->bstream_dirty = false;
-    }
-  }
+  int rc = join_tails(c, st, true);
+  if (rc) return rc;
   // ranks that left after this step's last bucket call: one barrier over the
   // mask they last took part in
-  int rc = ctx_transition(c, live_mask, st);
-  if (rc) return rc;
-  rc = ctx_barrier(c, live_mask, participate != 0, st);
-  if (rc) return rc;
-  rc = ctx_flush(c, st, -1);
-  if (rc) return rc;
+  if ((rc = ctx_transition(c, live_mask, st))) return rc;
+  // the closing barrier: every live peer finished every combine of the step
+  if ((rc = full_barrier(c, live_mask, participate != 0, st))) return rc;
+  if ((rc = ctx_flush(c, st, -1))) return rc;
   c->in_step = false;
   c->last_live = 0;  // the closing barrier synchronised every live rank
   return RCV_OK;
@@ -2674,17 +2921,10 @@ int rcv_ctx_finish(rcv_ctx *c, uint64_t live_mask, int participate, void *main_s
 
 int rcv_ctx_poll(rcv_ctx *c, uint64_t live_mask, int participate, void *main_stream) {
   cudaStream_t st = (cudaStream_t)main_stream;
-  if (c->in_step) {
-    CK(cudaEventRecord(c->ev_ready, c->side));
-    CK(cudaStreamWaitEvent(st, c->ev_ready, 0));
-    if (c->bstream_dirty) {
-      CK(cudaEventRecord(c->ev_ready, c->bstream));
-      CK(cudaStreamWaitEvent(st, c->ev_ready, 0));
-    }
-  }
-  int rc = ctx_transition(c, live_mask, st);
+  int rc = join_tails(c, st, false);
   if (rc) return rc;
-  return ctx_barrier(c, live_mask, participate != 0, st);
+  if ((rc = ctx_transition(c, live_mask, st))) return rc;
+  return full_barrier(c, live_mask, participate != 0, st);
 }
 
 int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
@@ -2814,12 +3054,16 @@ int rcv_plan_destroy(rcv_plan *p) {
   return RCV_OK;
 }
 
-// One bucket call j of the step (see include/rcv.h for the schedule).  Three
-// pool sets: call j's pre-reduce overwrites the set last read by the combine
-// of call j-3, which every peer finished before its barrier of call j-2.  So
-// the side stream only waits for that barrier and can run up to two buckets
-// ahead of the combines; the buckets combined at calls <= j-3 are then also
-// complete in this rank's primary.
+// One bucket call j of the step (see include/rcv.h for the schedule).  Four
+// streams: side (pre-reduces), bar (barriers), main (combines), bstream
+// (perfect covers' local broadcasts).  With barrier lag L (rcv_ctx::lag),
+// barrier j waits for this rank's pre-reduce j and its combine j-L, so
+// passing it proves every live peer finished both.  S pool sets
+// (rcv_pool_sets): call j's pre-reduce overwrites the set last read by
+// combine j-S, which every peer finished before its barrier j-S+L, so the
+// side stream waits only for that barrier and runs up to S-L-1 pre-reduces
+// ahead of the barriers; bucket b's outputs are complete in every primary
+// once barrier b+L passed (its local broadcast).
 int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
   if (n == 0) return RCV_OK;
   rcv_ctx *c = p->ctx;
@@ -2827,7 +3071,9 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
   // while timing launch by launch everything runs on the caller's stream, so
   // each kernel's duration is its own (no cross-stream overlap stretching it)
   cudaStream_t side = c->timing ? main : c->side;
+  cudaStream_t bar = bar_stream(c, main);
   const int es = esize(p->has_comb ? p->comb.acc_dt : RCV_F32);
+  const long long L = c->lag;
   if (!c->in_step) {
     // leaves were produced on the caller's stream
     c->in_step = true;
@@ -2837,23 +3083,25 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
   int rc = ctx_transition(c, p->live_mask, main);
   if (rc) return rc;
   const unsigned long long j = c->calls++;
-  const int set = (int)(j % 3);
+  const long long jj = (long long)j;
+  const unsigned long long S = (unsigned long long)c->sets;
+  const int set = (int)(j % S);
   const size_t set_off = set * p->set_stride;
   // perfect covers (pre-reduce-bound) broadcast on their own stream right
   // behind each barrier; fragmented ones (combine-bound) keep them on the
   // side stream, off the SMs the NVLink-bound combine needs
   // (profiles/r1f/schedule_ab.txt)
   const bool bstream = !c->timing && p->perfect;
-  if (j >= 2) {
-    CK(cudaStreamWaitEvent(side, c->ev_arrived[(j - 2) % 3], 0));
-    if (j >= 3 && !bstream) {
+  if (jj - (long long)S + L >= 0) {
+    CK(cudaStreamWaitEvent(side, c->ev_arrived[(j - S + L) % S], 0));
+    if (j >= S && !bstream) {
       if (c->bstream_dirty) {
         // an earlier broadcast of the same bucket may still be on bstream
         CK(cudaEventRecord(c->ev_bcast, c->bstream));
         CK(cudaStreamWaitEvent(side, c->ev_bcast, 0));
         c->bstream_dirty = false;
       }
-      if ((rc = ctx_flush(c, side, (long long)j - 3))) return rc;
+      if ((rc = ctx_flush(c, side, jj - (long long)S))) return rc;
     }
   }
   const bool writes = p->participate && (p->has_forest || !p->pre.empty()) && !c->no_stamps;
@@ -2879,8 +3127,11 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
       return rc;
   }
   if (writes && (rc = stamp_write(c, side, c->stamp_of(c->me, set), j + 1))) return rc;
-  CK(cudaEventRecord(c->ev_ready, side));
-  CK(cudaStreamWaitEvent(main, c->ev_ready, 0));
+  if (side != bar) {
+    CK(cudaEventRecord(c->ev_ready, side));
+    CK(cudaStreamWaitEvent(bar, c->ev_ready, 0));
+  }
+  if (bar != main && jj - L >= 0) CK(cudaStreamWaitEvent(bar, c->ev_comb[(j - L) % S], 0));
   size_t a = 0, z = 0;
   std::vector<const unsigned long long *> now;
   if (p->has_comb) {
@@ -2890,26 +3141,29 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
     if (z > a && !c->no_stamps)
       for (int rk : p->producers) now.push_back(c->stamp_of(rk, set));
   }
-  if ((rc = ctx_barrier(c, p->live_mask, p->participate, main, &now, j + 1))) return rc;
-  CK(cudaEventRecord(c->ev_arrived[j % 3], main));
-  if (bstream && j >= 1) {
-    // passing barrier j proves every peer finished combine j-1: the buckets
-    // combined at calls <= j-1 are complete in this rank's primary
-    CK(cudaStreamWaitEvent(c->bstream, c->ev_arrived[j % 3], 0));
-    if ((rc = ctx_flush(c, c->bstream, (long long)j - 1))) return rc;
+  // the barrier re-checks the stamps of the combines it is ordered behind
+  // (calls <= j-L; all earlier ones while timing on one stream)
+  if ((rc = ctx_barrier(c, p->live_mask, p->participate, bar, bar == main ? jj - 1 : jj - L, j,
+                        &now, j + 1)))
+    return rc;
+  CK(cudaEventRecord(c->ev_arrived[j % S], bar));
+  if (bar != main) CK(cudaStreamWaitEvent(main, c->ev_arrived[j % S], 0));
+  if (bstream && jj - L >= 0) {
+    // the buckets combined at calls <= j-L are complete in this rank's primary
+    CK(cudaStreamWaitEvent(c->bstream, c->ev_arrived[j % S], 0));
+    if ((rc = ctx_flush(c, c->bstream, jj - L))) return rc;
     c->bstream_dirty = true;
   }
   if (z > a) {
-    {
-      FoldReq r = p->comb;
-      shift(r, set_off + a, lo + a);
-      const double sl = (double)(z - a) * es;
-      const double local = (double)(r.n_in - p->remote_in + r.n_out - p->remote_out) * sl;
-      rc = timed(c, main, 3, local, p->remote_in * sl, p->remote_out * sl,
-                 [&]() { return run_fold(r, z - a, p->comb_variant, main, c->sms); });
-      if (rc) return rc;
-    }
+    FoldReq r = p->comb;
+    shift(r, set_off + a, lo + a);
+    const double sl = (double)(z - a) * es;
+    const double local = (double)(r.n_in - p->remote_in + r.n_out - p->remote_out) * sl;
+    rc = timed(c, main, 3, local, p->remote_in * sl, p->remote_out * sl,
+               [&]() { return run_fold(r, z - a, p->comb_variant, main, c->sms); });
+    if (rc) return rc;
   }
+  CK(cudaEventRecord(c->ev_comb[j % S], main));
   if (p->has_bcast) {
     rcv_ctx::Pending e;
     e.req = p->bcast;

@@ -416,13 +416,14 @@ class DistributedGradientCommit(GradientCommit):
             store, store_ptr = vb.share(per * self._slot * self._es, dtype)
             store.zero_()
         if real_kill:
-            self.pool, self.pool_ptr = vb.share(3 * pool_slots * self.lmax * self._es, dtype)
+            self.pool, self.pool_ptr = vb.share(_lib.pool_sets() * pool_slots * self.lmax * self._es, dtype)
             self.flags, self.flag_ptr = vb.share(FLAG_SLOTS * 8, torch.int64)
             self.flags.zero_()
         else:
             if not self.multicast:
                 store = torch.zeros(per * numel, dtype=dtype, device=self.device)
-            self.pool = torch.empty(3 * pool_slots * self.lmax, dtype=dtype, device=self.device)
+            self.pool = torch.empty(_lib.pool_sets() * pool_slots * self.lmax, dtype=dtype,
+                                        device=self.device)
             self.flags = torch.zeros(FLAG_SLOTS, dtype=torch.int64, device=self.device)
             pb = PeerBuffers(self.rank, self.world, group)
             if not self.multicast:
@@ -697,8 +698,7 @@ class DistributedGradientCommit(GradientCommit):
             # the native plan depends only on the leaf layout: which rank
             # holds which microbatch at which address, and the membership
             layout = (tuple(self.comm.members), self.state.b,
-                      tuple((m, rid, v.data_ptr(), v.dtype) if v is not None else (m, rid)
-                            for m, (rid, v) in sorted(leaves.items())))
+                      tuple((m, rid) + _value_key(v) for m, (rid, v) in sorted(leaves.items())))
             if not self.rt.use_cached(layout):
                 self._set_plan(leaves, layout)
             self._plan_key = (key, leaves)
@@ -709,6 +709,16 @@ class DistributedGradientCommit(GradientCommit):
         self.rt.bucket(lo, n, self._stream)
         self.host_prof["bucket_s"] += time.perf_counter() - h0
         return 1
+
+
+def _value_key(v) -> tuple:
+    """What a native plan captures of one leaf value: its address and dtype
+    (a microbatch gradient) or its subtree and address (a K-ACC node)."""
+    if v is None:
+        return ()
+    if isinstance(v, torch.Tensor):
+        return (v.data_ptr(), v.dtype)
+    return (v.lo, v.level, v.tensor.data_ptr(), v.tensor.dtype)
 
 
 def shard_bounds(numel: int, shards: int, align: int = 64):

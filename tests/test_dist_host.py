@@ -10,7 +10,11 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2605_11215_b200.commit import block_cover
-from paper_2605_11215_b200.dist import DistributedGradientCommit, owner_slice, plan_bucket
+import torch
+
+from paper_2605_11215_b200.dist import (DistributedGradientCommit, _value_key, owner_slice,
+                                        plan_bucket)
+from paper_2605_11215_b200.kacc import KNode
 
 
 def test_owner_slices_partition():
@@ -20,6 +24,18 @@ def test_owner_slices_partition():
             assert spans[0][0] == 0 and spans[-1][1] == n
             for (a, z), (a2, _) in zip(spans, spans[1:]):
                 assert z == a2 and a % 64 == 0
+
+
+def test_plan_cache_key_covers_every_leaf_kind():
+    # the native plan cache keys a leaf set by what the plan captures: a
+    # microbatch gradient's address, a K-ACC node's subtree and address
+    # (HSDP and the executor commit K-ACC nodes), nothing for a dead leaf
+    t = torch.zeros(4)
+    assert _value_key(None) == ()
+    assert _value_key(t) == (t.data_ptr(), torch.float32)
+    n = KNode(8, 2, t)
+    assert _value_key(n) == (8, 2, t.data_ptr(), torch.float32)
+    assert _value_key(KNode(12, 2, t)) != _value_key(n)
 
 
 def test_plan_failure_layout():

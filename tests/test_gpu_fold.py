@@ -94,11 +94,15 @@ def test_accumulate_order_and_canon(gdt):
              for _ in range(6)]
     grads[0][:5] = -0.0
     acc = torch.empty(numel, dtype=torch.float32, device=DEV)
-    for j, g in enumerate(grads):
-        _lib.accumulate(acc, g.to(DEV), first=(j == 0))
+    _lib.accumulate(acc, grads[0].to(DEV), first=True)
+    # the first round is `zeros + grad` (trainer.py:192, 212): -0.0 -> +0.0
+    assert not np.signbit(host(acc)[:5]).any()
+    assert host(acc).tobytes() == fold.local_accumulate([grads[0].float().numpy()],
+                                                        np.float32).tobytes()
+    for g in grads[1:]:
+        _lib.accumulate(acc, g.to(DEV), first=False)
     want = fold.local_accumulate([g.float().numpy() for g in grads], np.float32)
     assert host(acc).tobytes() == want.tobytes()
-    assert not np.signbit(host(acc)[:5]).any() or True
 
 
 def test_accumulate_f64():
@@ -225,19 +229,34 @@ def test_unit_lanes_bit_exact():
 
 
 @pytest.mark.multigpu
-def test_multidevice_allreduce():
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n_views", [2, 3, 8, 10])
+def test_multidevice_allreduce(dtype, n_views):
+    """The drop-in collective over views on several GPUs: <= 8 contributors
+    run the fused one-launch kernel (entry barrier, owner slice, exit
+    barrier), more take barrier + fold + barrier; bitwise vs the oracle's
+    ascending masked fold, with empty owner slices (numel < 8 per device),
+    ragged tails and the /B divisor."""
     n_dev = torch.cuda.device_count()
     _lib.enable_peer_access(list(range(n_dev)))
-    rng = np.random.default_rng(9)
-    for numel in (1, 1000, 1 << 20 | 3):
-        arrs = [rng.standard_normal(numel).astype(np.float32) for _ in range(8)]
-        contrib = [True, False, True, True, True, True, True, False]
-        want = fold.masked_fold(arrs, contrib)
-        views = [torch.from_numpy(a).to("cuda:%d" % (i % n_dev)) for i, a in enumerate(arrs)]
-        _lib.masked_allreduce(views, contrib)
-        for v in views:
-            torch.cuda.synchronize(v.device)
-            assert host(v).tobytes() == want.tobytes()
+    rng = np.random.default_rng(9 + n_views)
+    for numel in (1, 5, 1000, 1 << 20 | 3):
+        for divisor in (0.0, 3.0):
+            arrs = [rng.standard_normal(numel).astype(dtype) for _ in range(n_views)]
+            contrib = [i != 1 for i in range(n_views)]  # 10 views: 9 contributors
+            want = fold.masked_fold(arrs, contrib)
+            if divisor:
+                want = want / dtype(divisor)
+            views = [torch.from_numpy(a).to("cuda:%d" % (i % n_dev)) for i, a in enumerate(arrs)]
+            for _ in range(2):  # the second call re-reduces the first's output
+                _lib.masked_allreduce(views, contrib, divisor)
+                for v in views:
+                    torch.cuda.synchronize(v.device)
+                    assert host(v).tobytes() == want.tobytes(), (numel, divisor)
+                arrs = [host(v) for v in views]
+                want = fold.masked_fold(arrs, contrib)
+                if divisor:
+                    want = want / dtype(divisor)
 
 
 @pytest.mark.parametrize("variant", [_lib.VARIANT_AUTO, _lib.VARIANT_TMA, _lib.VARIANT_DIRECT])

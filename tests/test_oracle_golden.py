@@ -64,7 +64,8 @@ def test_fold_order_known_answer():
     # (1e16 + 1) + (-1e16) == 0 in ascending order (test_comm.py:235-243)
     v = [np.array([1e16]), np.array([1.0]), np.array([-1e16])]
     assert fold.masked_fold(v, [True] * 3)[0] == 0.0
-    assert fold.masked_fold(v[::-1], [True] * 3)[0] == 1.0 - 0.0 or True
+    # the order is the result: folding the -1e16 in before the 1.0 keeps it
+    assert fold.masked_fold([v[0], v[2], v[1]], [True] * 3)[0] == 1.0
 
 
 def test_canonical_tree_matches_blocks():
