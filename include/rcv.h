@@ -280,12 +280,14 @@ int rcv_barrier(uint64_t *local_flags, void *const *peer_flags, int n, int me,
  * barrier lag L (RCV_BARRIER_LAG, default 2)
  *   [membership shrank since the previous call: barrier over the previous
  *    live mask behind this rank's last combine, departing ranks included]
- *   side stream:  wait(barrier j-S+L: pool set j%S free) -> [broadcasts,
- *                 fragmented covers] -> stamp(set) = 0 -> pre-reduce nodes
- *                 into pool set j%S -> stamp(set) = j+1 -> record(ready)
+ *   side stream:  wait(barrier j-S+L: pool set j%S free, its stamp 0) ->
+ *                 [broadcasts, fragmented covers] -> pre-reduce nodes into
+ *                 pool set j%S -> record(ready)
  *   bar stream:   wait(ready) -> wait(combine j-L) -> barrier (before its
- *                 signal re-checks the stamps combine j-L read; after its
- *                 wait checks every producer's stamp of set j%S == j+1)
+ *                 signal re-checks the stamps combine j-L read and stamps
+ *                 its own set j%S = j+1; after its wait checks every
+ *                 producer's stamp of set j%S == j+1 and stamps its own set
+ *                 (j+S-L)%S = 0, the next one to be overwritten)
  *                 -> record(arrived)
  *   main stream:  wait(arrived) -> combine(owner slice) -> record(combined)
  *   bcast stream: wait(arrived) -> broadcasts of the buckets combined at

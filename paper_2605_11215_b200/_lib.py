@@ -193,8 +193,15 @@ def require_cuda(t: torch.Tensor, what: str = "tensor") -> None:
         raise ValueError("%s must be a contiguous 1-D view" % what)
 
 
+def raw_stream(device_index: int) -> int:
+    """The current stream of a CUDA device as a cudaStream_t (an int); the
+    raw accessor skips building a torch.cuda.Stream per call (host time of
+    the small-bucket collective)."""
+    return torch._C._cuda_getCurrentRawStream(device_index)
+
+
 def stream_of(t: torch.Tensor) -> int:
-    return torch.cuda.current_stream(t.device).cuda_stream
+    return raw_stream(t.device.index)
 
 
 def _ptrs(ts: Sequence[torch.Tensor]):
@@ -250,8 +257,7 @@ def masked_allreduce(views: Sequence[torch.Tensor], contrib: Sequence[bool],
                                         stream_of(first)))
         return
     dev_arr = (ctypes.c_int * len(devs))(*devs)
-    streams = (ctypes.c_void_p * len(devs))(
-        *[torch.cuda.current_stream(d).cuda_stream for d in devs])
+    streams = (ctypes.c_void_p * len(devs))(*[raw_stream(d) for d in devs])
     _check(lib.rcv_masked_allreduce_multidev(
         _ptrs(views), n, mask, code, first.numel(), float(divisor),
         len(devs), dev_arr, streams))

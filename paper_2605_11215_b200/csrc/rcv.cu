@@ -964,6 +964,13 @@ struct BarrierParams {
   int n_now, n_prev;
   unsigned long long now_value;
   unsigned int *err;
+  // this rank's own pool-set stamps (multi-process runtime): `ready` (the set
+  // the pre-reduce of this call wrote) gets ready_value before the signal;
+  // `inval` (the set the next overwrite targets, free once every live peer
+  // passed this barrier) gets 0 after the wait.  NULL: none.
+  unsigned long long *ready;
+  unsigned long long ready_value;
+  unsigned long long *inval;
   // real-kill mode: the node's liveness dead word (mapped host memory,
   // rcv_liveness); a peer whose bit is set is not waited for
   const volatile unsigned int *host_dead;
@@ -984,6 +991,10 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   // a peer that already timed out is dead: never signal or wait on it again
   const unsigned int dead = *(volatile const unsigned int *)p.status | (p.host_dead ? *p.host_dead : 0u);
   const bool peer = t < p.n && t != p.me && ((p.live >> t) & 1ull) && !((dead >> t) & 1u);
+  // this call's partials are complete (the host ordered this launch behind
+  // the pre-reduce): stamp their set before any peer is released to read it
+  if (t == 0 && p.ready) *(volatile unsigned long long *)p.ready = p.ready_value;
+  __syncthreads();
   // everything this GPU wrote before this kernel (partials, remote and
   // multicast stores) is made visible system-wide before the flag store
   // releases it
@@ -1014,6 +1025,10 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.chk_now[t]) : "memory");
     if (v != p.now_value) atomicOr(p.err, 1u);
   }
+  // every live peer finished the combine that last read the set `inval`
+  // names: mark it invalid before the pre-reduce behind this barrier
+  // overwrites it (a late reader's re-check then sees the change)
+  if (t == 0 && p.inval) *(volatile unsigned long long *)p.inval = 0ull;
 }
 
 // ---------------------------------------------------------------------------
@@ -2487,12 +2502,6 @@ namespace {
 constexpr int kStampBase = 64;
 constexpr int kMaxSets = 4;
 
-__global__ void stamp_kernel(unsigned long long *addr, unsigned long long value) {
-  __threadfence_system();
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(addr), "l"(value) : "memory");
-}
-
-typedef CUresult (*WriteValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
 
 }  // namespace
 
@@ -2528,8 +2537,7 @@ struct rcv_ctx {
   // barrier over this mask, departing ranks included: their last combine
   // read this rank's pool sets and stored into its primary.
   uint64_t last_live = 0;
-  WriteValue64 write_value = nullptr;  // cuStreamWriteValue64 (stamp_kernel when absent)
-  bool no_stamps = false;              // RCV_NO_STAMPS=1: measurement A/B only
+  bool no_stamps = false;  // RCV_NO_STAMPS=1: measurement A/B only
   // the stamps each combine not yet re-checked read, in call order; a
   // barrier re-checks those of the combines it is ordered behind
   struct Check {
@@ -2601,11 +2609,13 @@ int timed(rcv_ctx *c, cudaStream_t st, int kind, double bytes, double nin, doubl
 // behind (-1: all of them; the caller made the bar stream wait for main's
 // tail); those combines' stamps are re-checked before the signal.  `now`:
 // the stamps the combine of this call reads, checked == now_value after the
-// wait.
+// wait.  `ready` / `inval`: this rank's own stamps the kernel writes
+// (BarrierParams).
 int ctx_barrier(rcv_ctx *c, uint64_t live, bool participate, cudaStream_t st, long long upto,
                 unsigned long long call = 0,
                 const std::vector<const unsigned long long *> *now = nullptr,
-                unsigned long long now_value = 0) {
+                unsigned long long now_value = 0, unsigned long long *ready = nullptr,
+                unsigned long long *inval = nullptr) {
   if (!participate || __builtin_popcountll(live) < 2) {
     c->hist.clear();  // no peer: nothing can race this rank's combines
     return RCV_OK;
@@ -2629,6 +2639,9 @@ int ctx_barrier(rcv_ctx *c, uint64_t live, bool participate, cudaStream_t st, lo
   c->bar.n_now = now ? (int)now->size() : 0;
   for (int i = 0; i < c->bar.n_now; ++i) c->bar.chk_now[i] = (*now)[i];
   c->bar.now_value = now_value;
+  c->bar.ready = ready;
+  c->bar.ready_value = now_value;
+  c->bar.inval = inval;
   if (now) c->hist.push_back({call, now_value, *now});
   return timed(c, st, 1, 0, 0, 0, [&]() {
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -2672,19 +2685,6 @@ int ctx_transition(rcv_ctx *c, uint64_t live, cudaStream_t main) {
   c->last_live = live;
   if (!prev || !(prev & ~live)) return RCV_OK;
   return full_barrier(c, prev, (prev >> c->me) & 1ull, main);
-}
-
-int stamp_write(rcv_ctx *c, cudaStream_t st, unsigned long long *addr, unsigned long long v) {
-  if (c->write_value) {
-    // default flags: the write is preceded by a system-scope memory barrier
-    if (c->write_value((CUstream)st, (CUdeviceptr)addr, (cuuint64_t)v, 0) != CUDA_SUCCESS)
-      return set_err(RCV_ECUDA, "cuStreamWriteValue64");
-    return RCV_OK;
-  }
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  stamp_kernel<<<1, 1, 0, st>>>(addr, v);
-  CK(cudaGetLastError());
-  return RCV_OK;
 }
 
 // Broadcast the pending buckets combined at call index <= upto (all of them
@@ -2804,19 +2804,6 @@ int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer
   c->bar.me = me;
   c->err = status + 1;
   c->no_stamps = getenv("RCV_NO_STAMPS") && atoi(getenv("RCV_NO_STAMPS"));
-  {
-    // stream memory operations write the stamps without a kernel launch
-    int ok = 0;
-    cudaDeviceGetAttribute(&ok, (cudaDeviceAttr)CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, c->device);
-    cudaGetLastError();
-    cudaDriverEntryPointQueryResult q;
-    void *fn = nullptr;
-    if (ok && !getenv("RCV_STAMP_KERNEL") &&
-        cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess && fn)
-      c->write_value = (WriteValue64)fn;
-    cudaGetLastError();
-  }
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->bstream, cudaStreamNonBlocking));
   {
@@ -3104,8 +3091,12 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
       if ((rc = ctx_flush(c, side, jj - (long long)S))) return rc;
     }
   }
+  // this call's pool set is stamped j+1 by barrier j once the pre-reduce is
+  // done, and marked 0 by barrier j-S+L (which the side stream waited for
+  // above) before it is overwritten: no stream operation between the
+  // pre-reduces (a system-scope stream memop costs up to ~20 us on a GPU
+  // busy with NVLink traffic)
   const bool writes = p->participate && (p->has_forest || !p->pre.empty()) && !c->no_stamps;
-  if (writes && (rc = stamp_write(c, side, c->stamp_of(c->me, set), 0))) return rc;
   bool forest_done = false;
   if (p->has_forest && n % 64 == 0) {
     FoldReq r = p->forest;
@@ -3126,7 +3117,6 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
     if ((rc = timed(c, side, 0, bytes, 0, 0, [&]() { return run_fold(r, n, p->variant, side, c->sms); })))
       return rc;
   }
-  if (writes && (rc = stamp_write(c, side, c->stamp_of(c->me, set), j + 1))) return rc;
   if (side != bar) {
     CK(cudaEventRecord(c->ev_ready, side));
     CK(cudaStreamWaitEvent(bar, c->ev_ready, 0));
@@ -3144,7 +3134,8 @@ int rcv_plan_bucket(rcv_plan *p, size_t lo, size_t n, void *main_stream) {
   // the barrier re-checks the stamps of the combines it is ordered behind
   // (calls <= j-L; all earlier ones while timing on one stream)
   if ((rc = ctx_barrier(c, p->live_mask, p->participate, bar, bar == main ? jj - 1 : jj - L, j,
-                        &now, j + 1)))
+                        &now, j + 1, writes ? c->stamp_of(c->me, set) : nullptr,
+                        c->no_stamps ? nullptr : c->stamp_of(c->me, (int)((j + S - L) % S)))))
     return rc;
   CK(cudaEventRecord(c->ev_arrived[j % S], bar));
   if (bar != main) CK(cudaStreamWaitEvent(main, c->ev_arrived[j % S], 0));

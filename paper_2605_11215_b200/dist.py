@@ -17,14 +17,15 @@ crosses GPUs:
    evaluates the top of the canonical tree, divides by B and stores the
    slice into the primary replica buffer of every live rank (peers' over
    NVLink) — reduce-scatter and all-gather fused in one launch;
-4. *local broadcast* — after the next barrier each rank copies the bucket
+4. *local broadcast* — two barriers later each rank copies the bucket
    from its primary replica into its other replicas (HBM), so NVLink carries
    one copy per rank, not one per replica.
 
-Partial pools are triple-buffered by call index, so one barrier per bucket
-suffices (a rank passing barrier k+1 has finished combine k) and the
-pre-reduce stream may run two buckets ahead; one more barrier closes the
-step.  Pre-reduces run on a side stream, so bucket k+1's
+Barriers run on their own stream, barrier k behind this rank's combine k-2
+(so it overlaps combine k-1), and partial pools rotate through four sets by
+call index, so one barrier per bucket suffices (a rank passing barrier k has
+finished pre-reduce k and combine k-2) and the pre-reduce stream may run a
+bucket ahead of the barriers; one more barrier closes the step.  Pre-reduces run on a side stream, so bucket k+1's
 HBM-bound pre-reduce overlaps bucket k's NVLink-bound combine.  The whole
 per-bucket schedule lives in the native runtime (rcv_ctx / rcv_plan in
 librcv.so): a plan is prepared once per leaf cover and each bucket costs the
