@@ -998,6 +998,8 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   // everything this GPU wrote before this kernel (partials, remote and
   // multicast stores) is made visible system-wide before the flag store
   // releases it
+  // (fence cost is not on the critical path: release/acquire-only and
+  // relaxed flag accesses measured the same, gpurun_out/r2s)
   asm volatile("fence.proxy.alias;" ::: "memory");
   __threadfence_system();
   if (peer)
@@ -3029,7 +3031,12 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
     for (int j = 0; j < d->n_bcast; ++j) r.out[j] = (char *)d->bcast_out[j];
     r.full_L = 0;  // a one-leaf tree: the straight-line DIRECT (256-bit) copy
     r.acc_dt = d->acc_dtype;
-    r.max_ctas = env_ctas("RCV_BCAST_CTAS", ctx->sms, 0.0);
+    // one copy per bucket (two replicas per rank) runs beside the combine
+    // and the next pre-reduce: 0.3 of the SMs leaves them their share
+    // (N=4 failure-free step 1.85 -> 1.60 ms); several copies (N=2: three)
+    // are the HBM-bound part of the step and run uncapped
+    // (profiles/r2/bcast_cap_ab.txt)
+    r.max_ctas = env_ctas("RCV_BCAST_CTAS", ctx->sms, d->n_bcast == 1 ? 0.3 : 0.0);
     p->has_bcast = true;
   }
   *out = p;

@@ -7,7 +7,9 @@ the same protocol point (first rank to reach a poll decides it) and recover
 in-step (boundary extension, re-reduce over the survivors).  Every committed
 gradient on every survivor — before, during and after the failure — is
 bitwise the CPU oracle's canonical tree, i.e. the failure-free result; no
-step is rolled back or replayed.  Ranks share GPUs on smaller boxes."""
+step is rolled back or replayed.  One GPU per rank (two spinning ranks on
+one GPU risk a context-switch timeout, B200_PROFILING.md), so it needs >= 2
+devices."""
 
 import os
 import signal
@@ -18,7 +20,7 @@ import torch
 
 from mp_util import free_port, init_rank
 
-pytestmark = [pytest.mark.gpu]
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 
 def _worker(rank, world, port, q):
@@ -73,7 +75,8 @@ def test_real_process_death_recovered_in_step():
         p.join(timeout=60)
         if p.is_alive():
             p.kill()
-    assert procs[1].exitcode == -signal.SIGKILL          # the victim really died
+    # the victim really died (its traceback is in `got` if it raised instead)
+    assert procs[1].exitcode == -signal.SIGKILL, got.get(1)
     assert sorted(got) == [r for r in range(world) if r != 1]
     b = 4 * world
     points = set()
