@@ -179,3 +179,52 @@ def test_committed_buckets_survive_boundary(monkeypatch, bucket):
     # relaunches only the failed bucket and those after it
     assert a.boundary_crossed and z.boundary_crossed
     assert z.launches - a.launches == bucket
+
+
+def test_full_size_configs1_failure_step_vs_torch_tree():
+    """configs[1] at full size: the GPT-2 124M gradient (d = 124,439,808
+    fp32), 8 replicas x 4 microbatches, 20 buckets, replica 3 killed during
+    the sync of bucket 7.  The survivors regenerate the dead replica's
+    microbatch gradients (their own buffers, the same seeded values) and every
+    survivor's committed gradient must equal, bitwise, the canonical tree
+    evaluated independently with plain torch fp32 adds level by level and a
+    true division by 32 (no librcv on the reference side) — at every element.
+    The next step (the advanced 7-replica layout) commits the same bits."""
+    d, w, g, k = 124_439_808, 8, 4, 20
+    b = w * g
+
+    def make(m):
+        gen = torch.Generator(device=DEV).manual_seed(4321 + m)
+        return torch.randn(d, generator=gen, device=DEV, dtype=torch.float32)
+
+    leaves = [make(m) for m in range(b)]
+    regen = {}
+
+    def leaf(m, rid):
+        if m // g == 3 and rid != 3:          # taken over from the dead replica
+            if m not in regen:
+                regen[m] = make(m)
+            return regen[m]
+        return leaves[m]
+
+    eng = GradientCommit(d, w, g, k)
+    out = eng.step(0, leaf, Scripted([("during_sync", 7, [3])]))
+    assert out.contrib_total == b and out.events[0]["failed"] == [3]
+    assert sorted(regen) == [12, 13, 14, 15]
+    torch.cuda.synchronize()
+    chunk = 1 << 24
+    for step in (0, 1):
+        if step == 1:
+            eng.step(1, leaf)
+            torch.cuda.synchronize()
+        for lo in range(0, d, chunk):
+            hi = min(d, lo + chunk)
+            vals = [t[lo:hi] for t in leaves]
+            while len(vals) > 1:
+                vals = [vals[i] + vals[i + 1] for i in range(0, len(vals), 2)]
+            want = (vals[0] / float(b)).view(torch.int32)
+            for r in eng.comm.members:
+                bad = int((eng.grads[r][lo:hi].view(torch.int32) != want).sum())
+                assert bad == 0, (step, r, lo, bad)
+    del leaves, regen
+    torch.cuda.empty_cache()
