@@ -120,6 +120,10 @@ class HSDPTrainer:
             return done[m]
 
         out: CommitOutcome = self.engine.step(t, leaf, injector)
+        # per-microbatch losses of this replica's computations (the run's
+        # committed loss is the fold over all replicas' admitted ones)
+        self.last_losses = {m: float(v) for m, v in losses.items()
+                            if m in out.admitted.get(self.replica, ())}
         for p in self.params:
             p.grad = None
         loss = float("nan")

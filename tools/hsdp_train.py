@@ -74,6 +74,7 @@ def worker(rank, world, a, fail):
         out, loss = tr.step(t, kill)
         torch.cuda.synchronize()
         rows.append({"step": t, "wall_ms": (time.perf_counter() - t0) * 1e3, "loss": loss,
+                     "losses_by_m": {str(m): v for m, v in tr.last_losses.items()},
                      "contrib_total": out.contrib_total, "w_cur": out.w_cur,
                      "computed": sum(1 for s, _ in tr.computed if s == t)})
     import hashlib
@@ -107,6 +108,22 @@ def main():
         print(json.dumps({"failed": failed(got)}))
         sys.exit(1)
     surv = [r for r in range(world) if got[r]["alive"]]
+
+    def committed_losses(run):
+        """Per step: the mean over all 32 committed microbatch losses, folded
+        in microbatch-index order from whichever replica admitted each one
+        (every shard rank of a replica reports the same values)."""
+        out = []
+        for t in range(a.steps):
+            by_m = {}
+            for r in range(world):
+                by_m.update({int(m): v for m, v in run[r]["rows"][t]["losses_by_m"].items()})
+            tot = 0.0
+            for m in sorted(by_m):
+                tot += by_m[m]
+            out.append({"loss": tot / len(by_m), "microbatches": len(by_m)})
+        return out
+    loss_ref, loss_got = committed_losses(ref), committed_losses(got)
     same = all(got[r]["params_hash"] == ref[r]["params_hash"] for r in surv)
     steady = sorted(x["wall_ms"] for x in ref[0]["rows"][1:])
     doc = {
@@ -123,6 +140,10 @@ def main():
         "computed_by_replica0": [x["computed"] for x in got[0]["rows"]],
         "survivor_params_bitwise_equal_failure_free": same,
         "kacc_slots_per_rank": got[0]["kacc_slots"],
+        "committed_loss_failure_free": [x["loss"] for x in loss_ref],
+        "committed_loss_with_failure": [x["loss"] for x in loss_got],
+        "committed_loss_microbatches": [x["microbatches"] for x in loss_got],
+        "loss_trajectory_bitwise_equal": [x["loss"] for x in loss_ref] == [x["loss"] for x in loss_got],
         "losses_replica0_failure_free": [x["loss"] for x in ref[0]["rows"]],
         "losses_replica0_with_failure": [x["loss"] for x in got[0]["rows"]],
     }

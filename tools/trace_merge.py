@@ -17,7 +17,9 @@ def label(name):
     if base in SHORT:
         return SHORT[base]
     if "ProgFull<0>" in f:
-        return "bcast"
+        return "copy"
+    if "ProgFixed" in f:
+        return "COMB-fixed"
     if "Forest" in f or "ProgFull<3>" in f or "ProgFull<4>" in f:
         return "pre"
     return f[:18]
@@ -27,7 +29,8 @@ def main(paths, start_frac=0.5, count=60):
     ks = []
     for r, p in enumerate(paths):
         ev = json.load(open(p))["traceEvents"]
-        ks += [(e["ts"], e["ts"] + e["dur"], r, label(e["name"])) for e in ev if e.get("cat") == "kernel"]
+        ks += [(e["ts"], e["ts"] + e["dur"], r, "%s s%s" % (label(e["name"]), e["args"].get("stream")))
+               for e in ev if e.get("cat") == "kernel"]
     ks.sort()
     i0 = int(len(ks) * start_frac)
     t0 = ks[i0][0]
