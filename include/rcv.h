@@ -311,7 +311,7 @@ typedef struct rcv_ctx rcv_ctx;
 typedef struct rcv_plan rcv_plan;
 
 /* Number S of partial-pool sets a context rotates through (4; the
- * RCV_POOL_SETS=3 measurement switch gives 3). */
+ * RCV_POOL_SETS measurement switch takes 3..8). */
 int rcv_pool_sets(void);
 
 int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags,

@@ -2502,7 +2502,7 @@ namespace {
 // pool-set integrity stamps live in the rank's flag array after the barrier
 // slots: word kStampBase + s belongs to pool set s (rcv_pool_sets() sets)
 constexpr int kStampBase = 64;
-constexpr int kMaxSets = 4;
+constexpr int kMaxSets = 8;
 
 
 }  // namespace
@@ -2778,10 +2778,10 @@ double comb_share(const rcv_plan_desc *d) {
 extern "C" {
 
 int rcv_pool_sets(void) {
-  // RCV_POOL_SETS (3 or 4) is a measurement A/B; the allocator (dist.py)
-  // and the context read the same value
+  // RCV_POOL_SETS (3..8) is a measurement A/B; the allocator (dist.py) and
+  // the context read the same value
   const char *v = getenv("RCV_POOL_SETS");
-  return v && atoi(v) == 3 ? 3 : kMaxSets;
+  return v ? std::min(kMaxSets, std::max(3, atoi(v))) : 4;
 }
 
 int rcv_ctx_create(int n_ranks, int me, uint64_t *local_flags, void *const *peer_flags,
