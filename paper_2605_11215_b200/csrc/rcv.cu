@@ -2752,15 +2752,16 @@ int preload_module_kernels() {
   return RCV_OK;
 }
 
-// SM shares of the two concurrent streams (profiles/r1/caps_sweep.txt): the
-// NVLink-bound combine saturates the links with about a third of the SMs,
-// and a full-occupancy grid of either kernel would keep the other off the
-// GPU until its last wave drains.  Fragmented covers: combine 0.35 /
-// pre-reduce 0.65.  A perfect cover (one node per live rank, the
-// failure-free layout) moves the fewest NVLink bytes per HBM byte of
-// pre-reduce, so the pre-reduce sets the cadence and gets 0.75
-// (profiles/r1f/schedule_ab.txt).  RCV_COMB_CTAS / RCV_PRE_CTAS override
-// (an absolute CTA count > 2, or a fraction of the SMs; 0: uncapped).
+// SM shares of the concurrent streams: a full-occupancy grid of any kernel
+// would keep the others off the GPU until its last wave drains.  Pre-reduce:
+// 0.65 of the SMs for fragmented covers, 0.75 for a perfect cover (one node
+// per live rank, the failure-free layout: the pre-reduce sets the cadence,
+// profiles/r1f/schedule_ab.txt).  Combine: its owner slice shrinks as 1/n
+// with n live ranks, so its share does too, 0.45/n but at least 0.15 (N=2
+// 0.225, N=4 0.15: N=4 60.1 -> 63.1 M tokens/s against round 2's fixed
+// 0.25 / 0.35, N=2 56.9 -> 57.2 M; profiles/r2/comb_share_ab.txt).
+// RCV_COMB_CTAS / RCV_PRE_CTAS override (an absolute CTA count > 2, or a
+// fraction of the SMs; 0: uncapped).
 int env_ctas(const char *name, int sms, double dflt_frac) {
   const char *v = getenv(name);
   const double f = v ? atof(v) : dflt_frac;
@@ -2769,8 +2770,12 @@ int env_ctas(const char *name, int sms, double dflt_frac) {
   return std::max(1, (int)(f * sms));
 }
 
+double pre_share(const rcv_plan_desc *d) {
+  return d->n_comb > 0 && d->n_comb == d->slice_nr ? 0.75 : 0.65;
+}
+
 double comb_share(const rcv_plan_desc *d) {
-  return d->n_comb > 0 && d->n_comb == d->slice_nr ? 0.25 : 0.35;
+  return std::max(0.15, 0.45 / std::max(1, d->slice_nr));
 }
 
 }  // namespace
@@ -2927,7 +2932,7 @@ int rcv_plan_create(rcv_ctx *ctx, const rcv_plan_desc *d, rcv_plan **out) {
   p->perfect = d->n_comb > 0 && d->n_comb == d->slice_nr;
   p->remote_in = d->remote_in;
   p->remote_out = d->remote_out;
-  const int pre_ctas = env_ctas("RCV_PRE_CTAS", ctx->sms, 1.0 - comb_share(d));
+  const int pre_ctas = env_ctas("RCV_PRE_CTAS", ctx->sms, pre_share(d));
   int off = 0;
   for (int i = 0; i < d->n_pre; ++i) {
     FoldReq r;
