@@ -2753,13 +2753,13 @@ int preload_module_kernels() {
 }
 
 // SM shares of the concurrent streams: a full-occupancy grid of any kernel
-// would keep the others off the GPU until its last wave drains.  Pre-reduce:
-// 0.65 of the SMs for fragmented covers, 0.75 for a perfect cover (one node
-// per live rank, the failure-free layout: the pre-reduce sets the cadence,
-// profiles/r1f/schedule_ab.txt).  Combine: its owner slice shrinks as 1/n
-// with n live ranks, so its share does too, 0.45/n but at least 0.15 (N=2
-// 0.225, N=4 0.15: N=4 60.1 -> 63.1 M tokens/s against round 2's fixed
-// 0.25 / 0.35, N=2 56.9 -> 57.2 M; profiles/r2/comb_share_ab.txt).
+// would keep the others off the GPU until its last wave drains, and more
+// CTAs streaming HBM at once lower its efficiency.  Pre-reduce: 0.6 of the
+// SMs (N=4 62.7 -> 64.2 M tokens/s, N=2 56.1 -> 57.9 M against round 2's
+// 0.75 / 0.65; 0.3-0.5 and 0.85 are slower: profiles/r2/pre_share_ab.txt).
+// Combine: its owner slice shrinks as 1/n with n live ranks, so its share
+// does too, 0.45/n but at least 0.15 (N=2 0.225, N=4 0.15: N=4 60.1 -> 63.1
+// M against round 2's fixed 0.25 / 0.35; profiles/r2/comb_share_ab.txt).
 // RCV_COMB_CTAS / RCV_PRE_CTAS override (an absolute CTA count > 2, or a
 // fraction of the SMs; 0: uncapped).
 int env_ctas(const char *name, int sms, double dflt_frac) {
@@ -2770,9 +2770,7 @@ int env_ctas(const char *name, int sms, double dflt_frac) {
   return std::max(1, (int)(f * sms));
 }
 
-double pre_share(const rcv_plan_desc *d) {
-  return d->n_comb > 0 && d->n_comb == d->slice_nr ? 0.75 : 0.65;
-}
+double pre_share(const rcv_plan_desc *) { return 0.6; }
 
 double comb_share(const rcv_plan_desc *d) {
   return std::max(0.15, 0.45 / std::max(1, d->slice_nr));
