@@ -667,16 +667,38 @@ def e2e_leg(args, dev, leaves, numel, world=1):
         host[m].copy_(leaves[m])
     out_host = torch.empty(numel, dtype=torch.float32, pin_memory=pinned)
     stream = torch.cuda.current_stream(dev)
+    # copies on their own streams, pipelined across steps: step s+1's inputs
+    # go host->device on two copy streams (two copy engines) as soon as step
+    # s's commit has read its inputs, while step s's result comes back
+    # device->host on a third (PCIe is full duplex); step s+1's commit waits
+    # for its inputs and for that read-back (it rewrites the gradient)
+    h2d = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    d2h = torch.cuda.Stream(dev)
+    ev = {"commit": None, "d2h": None}
 
     kill = StepKill(-1 if args.no_fail else 1 + args.e2e_steps // 2,
                     min(VICTIM_BUCKET, args.buckets - 1))
 
     def one(s):
-        for m in idx:
-            leaves[m].copy_(host[m], non_blocking=True)
+        for cs in h2d:
+            if ev["commit"] is not None:
+                cs.wait_event(ev["commit"])
+        for i, m in enumerate(idx):
+            with torch.cuda.stream(h2d[i % 2]):
+                leaves[m].copy_(host[m], non_blocking=True)
+        for cs in h2d:
+            stream.wait_stream(cs)
+        if ev["d2h"] is not None:
+            stream.wait_event(ev["d2h"])
         kill.step = s
         eng.step(s, lambda m, rid: leaves[m], kill)
-        out_host.copy_(eng.grads[mine[0]], non_blocking=True)
+        ev["commit"] = torch.cuda.Event()
+        ev["commit"].record(stream)
+        d2h.wait_event(ev["commit"])
+        with torch.cuda.stream(d2h):
+            out_host.copy_(eng.grads[mine[0]], non_blocking=True)
+        ev["d2h"] = torch.cuda.Event()
+        ev["d2h"].record(d2h)
 
     one(0)
     torch.cuda.synchronize()
@@ -685,8 +707,10 @@ def e2e_leg(args, dev, leaves, numel, world=1):
     a = torch.cuda.Event(enable_timing=True)
     z = torch.cuda.Event(enable_timing=True)
     a.record(stream)
+    ev["commit"] = a  # the first copies start inside the timed region
     for s in range(args.e2e_steps):
         one(s + 1)
+    stream.wait_event(ev["d2h"])
     z.record(stream)
     torch.cuda.synchronize()
     ms = a.elapsed_time(z) / args.e2e_steps
