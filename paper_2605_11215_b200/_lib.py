@@ -231,6 +231,37 @@ def fold(inputs: Sequence[torch.Tensor], ops: Sequence[int],
                            stream if stream is not None else stream_of(acc)))
 
 
+# prepared arguments of the drop-in collective by call signature (every
+# view's address, length, dtype and stride, the contributor mask): a bucket
+# reduced again (every step, every re-reduce) skips validation and argument
+# marshalling (host time of the small-bucket collective)
+_ar_cache: "OrderedDict" = OrderedDict()
+
+
+class _ArgsAR:
+    __slots__ = ("multi", "ptrs", "n", "code", "numel", "devs", "dev_arr", "first_dev")
+
+
+def _prepare_allreduce(views, n, mask):
+    first = views[0]
+    for v in views:
+        require_cuda(v, "bucket view")
+        if v.dtype != first.dtype or v.numel() != first.numel():
+            raise ValueError("bucket views differ in dtype or length")
+    code = dtype_code(first)
+    if code == BF16:
+        raise TypeError("bucket views hold accumulators: float32 or float64")
+    a = _ArgsAR()
+    a.ptrs, a.n, a.code, a.numel = _ptrs(views), n, code, first.numel()
+    a.devs = sorted({v.device.index for v in views})
+    a.multi = len(a.devs) > 1
+    a.first_dev = first.device.index
+    if a.multi:
+        enable_peer_access(a.devs)
+        a.dev_arr = (ctypes.c_int * len(a.devs))(*a.devs)
+    return a
+
+
 def masked_allreduce(views: Sequence[torch.Tensor], contrib: Sequence[bool],
                      divisor: float = 0.0) -> None:
     """rcv_masked_allreduce (same device) or the multi-device variant."""
@@ -238,29 +269,29 @@ def masked_allreduce(views: Sequence[torch.Tensor], contrib: Sequence[bool],
     n = len(views)
     if n == 0:
         return
-    first = views[0]
-    for v in views:
-        require_cuda(v, "bucket view")
-        if v.dtype != first.dtype or v.numel() != first.numel():
-            raise ValueError("bucket views differ in dtype or length")
     mask = 0
     for i, c in enumerate(contrib):
         if c:
             mask |= 1 << i
-    code = dtype_code(first)
-    if code == BF16:
-        raise TypeError("bucket views hold accumulators: float32 or float64")
-    devs = sorted({v.device.index for v in views})
-    if len(devs) == 1:
-        _check(lib.rcv_masked_allreduce(_ptrs(views), n, mask, code,
-                                        first.numel(), float(divisor),
-                                        stream_of(first)))
+    try:
+        key = (mask, tuple([(v.data_ptr(), v.numel(), v.dtype, v.stride(0), v.is_cuda)
+                            for v in views]))
+    except (AttributeError, RuntimeError, IndexError):
+        key = None  # not tensors / not 1-D: the full checks raise the right error
+    a = _ar_cache.get(key) if key is not None else None
+    if a is None:
+        a = _prepare_allreduce(views, n, mask)
+        if key is not None:
+            _ar_cache[key] = a
+            if len(_ar_cache) > 256:
+                _ar_cache.popitem(last=False)
+    if not a.multi:
+        _check(lib.rcv_masked_allreduce(a.ptrs, n, mask, a.code, a.numel, float(divisor),
+                                        raw_stream(a.first_dev)))
         return
-    dev_arr = (ctypes.c_int * len(devs))(*devs)
-    streams = (ctypes.c_void_p * len(devs))(*[raw_stream(d) for d in devs])
-    _check(lib.rcv_masked_allreduce_multidev(
-        _ptrs(views), n, mask, code, first.numel(), float(divisor),
-        len(devs), dev_arr, streams))
+    streams = (ctypes.c_void_p * len(a.devs))(*[raw_stream(d) for d in a.devs])
+    _check(lib.rcv_masked_allreduce_multidev(a.ptrs, n, mask, a.code, a.numel, float(divisor),
+                                             len(a.devs), a.dev_arr, streams))
 
 
 _peer_done: set = set()
