@@ -97,3 +97,13 @@ def test_cpu_tensors_fail_loudly():
         _lib.accumulate(a, a)
     with pytest.raises(_lib.RcvError):
         _lib.masked_allreduce([a, a], [True, True])
+
+
+def test_pool_sets_switch(monkeypatch):
+    """rcv_pool_sets: the partial-pool set count the allocator (dist.py) and
+    the native runtime share; 4 by default, RCV_POOL_SETS clamped to 3..8."""
+    monkeypatch.delenv("RCV_POOL_SETS", raising=False)
+    assert _lib.pool_sets() == 4
+    for v, want in (("3", 3), ("6", 6), ("8", 8), ("20", 8), ("1", 3)):
+        monkeypatch.setenv("RCV_POOL_SETS", v)
+        assert _lib.pool_sets() == want, v
