@@ -679,15 +679,21 @@ def e2e_leg(args, dev, leaves, numel, world=1):
     kill = StepKill(-1 if args.no_fail else 1 + args.e2e_steps // 2,
                     min(VICTIM_BUCKET, args.buckets - 1))
 
+    # BENCH_E2E_COPY=serial: every copy on the step's stream (A/B only)
+    serial = os.environ.get("BENCH_E2E_COPY", "") == "serial"
+    if serial:
+        h2d, d2h = [stream, stream], stream
+
     def one(s):
         for cs in h2d:
-            if ev["commit"] is not None:
+            if ev["commit"] is not None and cs is not stream:
                 cs.wait_event(ev["commit"])
         for i, m in enumerate(idx):
             with torch.cuda.stream(h2d[i % 2]):
                 leaves[m].copy_(host[m], non_blocking=True)
         for cs in h2d:
-            stream.wait_stream(cs)
+            if cs is not stream:
+                stream.wait_stream(cs)
         if ev["d2h"] is not None:
             stream.wait_event(ev["d2h"])
         kill.step = s
