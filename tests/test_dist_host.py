@@ -79,24 +79,32 @@ def _worker(rank, world, port, q):
     q.put((rank, got))
 
 
-def test_replicated_plan_agrees_world2():
+@pytest.mark.parametrize("world", [2, 4])
+def test_replicated_plan_agrees(world):
+    """Every rank of a gloo group runs the replicated control plane through
+    replica 3's death and builds the bucket plan: identical decisions, cover
+    and slots on every rank, owner slices that partition the bucket."""
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=120) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    a, b = res[0][0], res[0][1]
-    assert a[:4] == b[:4]                 # same decision and plan on both ranks
-    assert a[0] == 28 and a[1] is True    # census of 7 survivors x 4
-    assert a[4][1] == b[4][0] and a[4][0] == 0 and b[4][1] == 6221990
+    views = res[0]
+    for v in views[1:]:
+        assert v[:4] == views[0][:4]      # same decision and plan on every rank
+    assert views[0][0] == 28 and views[0][1] is True    # census of 7 survivors x 4
+    spans = [v[4] for v in views]
+    assert spans[0][0] == 0 and spans[-1][1] == 6221990
+    for (a, z), (a2, _) in zip(spans, spans[1:]):
+        assert z == a2 and a % 64 == 0
 
 
 def test_dyadic_packing_minimises_cover():
